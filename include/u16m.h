@@ -1,0 +1,117 @@
+/* u16m — B200-native ill-formed UTF-16 repair, C ABI.
+ *
+ * Drop-in boundary for the reference's repair path (utf16mend). Every entry
+ * point computes exactly the reference's to_well_formed semantics: a high
+ * surrogate (D800-DBFF) not followed by a low surrogate, and a low surrogate
+ * (DC00-DFFF) not preceded by a high surrogate, becomes U+FFFD; every other
+ * unit is copied unchanged (reference SPEC.md:67-77).
+ *
+ * Conventions
+ *   - uint16_t is layout-identical to the reference's char16_t.
+ *   - Argument order is (in, n, out), the north-star order. The reference's
+ *     lower-level pointer forms are out-first (fix_scalar(out,in,n),
+ *     proj/src/bitmask_kernel_avx512.cpp:63); those are not exported.
+ *   - `out` must equal `in` exactly or not overlap it at all
+ *     (proj/src/driver.cpp:139-140); partial overlap -> U16M_ERR_ALIAS.
+ *   - Device entry points take device-accessible pointers and a CUDA stream
+ *     (cudaStream_t / CUstream passed as void*; NULL = legacy default stream).
+ *     They are asynchronous and stream-ordered; nothing is allocated.
+ *   - There is no CPU fallback: without a CUDA device every compute entry
+ *     point returns U16M_ERR_NO_DEVICE.
+ *   - Errors never throw across the ABI. u16m_last_error() returns a
+ *     thread-local detail string for the most recent failure on this thread.
+ */
+#ifndef U16M_H
+#define U16M_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define U16M_API_VERSION 1
+
+typedef enum u16m_status {
+  U16M_OK = 0,
+  U16M_ERR_INVALID_ARGUMENT = 1, /* null pointer with n>0, bad offsets, ...     */
+  U16M_ERR_ALIAS = 2,            /* in/out overlap partially                    */
+  U16M_ERR_NOT_DEVICE_MEMORY = 3,/* device entry point got a host pointer      */
+  U16M_ERR_CUDA = 4,             /* a CUDA runtime call or launch failed        */
+  U16M_ERR_MISALIGNED = 5,       /* pointer not 2-byte aligned                  */
+  U16M_ERR_NO_DEVICE = 6         /* no CUDA device visible                      */
+} u16m_status;
+
+/* Replaces: utf16mend::to_well_formed(span<const char16_t>, span<char16_t>,
+ * optional<kernel_id>) — proj/include/utf16mend/driver.hpp:64-65,
+ * proj/src/driver.cpp:135-142. Device pointers, async on `stream`. */
+u16m_status u16m_to_well_formed(const uint16_t* in, size_t n, uint16_t* out, void* stream);
+
+/* Replaces: utf16mend::to_well_formed_in_place(span<char16_t>, ...) —
+ * proj/include/utf16mend/driver.hpp:68-69, proj/src/driver.cpp:144-147. */
+u16m_status u16m_to_well_formed_in_place(uint16_t* buf, size_t n, void* stream);
+
+/* NEW (north star item 4; no reference function): each string
+ * [offsets[s], offsets[s+1]) for s < num_strings is repaired independently —
+ * string edges are "outside", so no pairing across strings. `offsets` is a
+ * DEVICE array of num_strings+1 non-decreasing int64 unit indices into
+ * in/out; units outside [offsets[0], offsets[num_strings]) are untouched.
+ * out may equal in. */
+u16m_status u16m_to_well_formed_batched(const uint16_t* in, const int64_t* offsets,
+                                        size_t num_strings, uint16_t* out, void* stream);
+
+/* One contiguous piece of a larger logical buffer (the per-shard primitive for
+ * one-process-per-GPU callers). `left`/`right` are the units just outside
+ * [0,n) in the logical buffer, or -1 where the logical buffer ends. Device
+ * pointers, async. */
+u16m_status u16m_to_well_formed_halo(const uint16_t* in, size_t n, uint16_t* out, int32_t left,
+                                     int32_t right, void* stream);
+
+/* Same, but the neighbour units are read on the device from `left_ptr` /
+ * `right_ptr` (any device-accessible address: local, or a peer GPU's memory
+ * over NVLink with peer access enabled); NULL = logical buffer ends there. */
+u16m_status u16m_to_well_formed_halo_ptr(const uint16_t* in, size_t n, uint16_t* out,
+                                         const uint16_t* left_ptr, const uint16_t* right_ptr,
+                                         void* stream);
+
+/* NEW (north star item 5): one logical buffer split into contiguous shards
+ * resident on (possibly) different GPUs of this process. Shard g lives on
+ * device device_ids[g]; shard_out[g] == shard_in[g] for in-place. Halo units
+ * cross shard edges as direct peer loads over NVLink when peer access is
+ * available, else through a 2-byte peer copy. Synchronous: returns when every
+ * shard is repaired. Device ids may repeat (virtual shards on one GPU). */
+u16m_status u16m_to_well_formed_sharded(int num_shards, const int* device_ids,
+                                        const uint16_t* const* shard_in, const size_t* shard_len,
+                                        uint16_t* const* shard_out);
+
+/* Host-memory form behind the source-compatible C++ API: stages through the
+ * current device in pipelined chunks (H2D / repair / D2H overlapped across
+ * streams). Synchronous. Pinned host memory gets full-duplex DMA. */
+u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out);
+
+/* §8(f) row 1 — validation. Device pointers. `count_out` (device, uint64) gets
+ * the number of units repair would rewrite; is_well_formed <=> count == 0.
+ * Async; the caller reads count_out after synchronising `stream`. */
+u16m_status u16m_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
+                                void* stream);
+
+/* Replaces: unpaired_surrogate_offsets(span, limit) (call sites
+ * proj/bindings/module.cpp:72-78, proj/tools/main.cpp:104). Writes up to
+ * `limit` ascending unit offsets to `offsets_out` (device) and the number
+ * written to *count_out (device). Async. */
+u16m_status u16m_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
+                                  unsigned long long* offsets_out,
+                                  unsigned long long* count_out, void* stream);
+
+const char* u16m_status_string(u16m_status status);
+const char* u16m_last_error(void);
+int u16m_api_version(void);
+/* Number of kernel launches this process has issued through the library
+ * (bench evidence: the "gpu_launches" count). */
+unsigned long long u16m_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* U16M_H */

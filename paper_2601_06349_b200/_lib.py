@@ -1,0 +1,317 @@
+"""ctypes binding of libu16m.so (include/u16m.h, include/u16m_datagen.h).
+
+Mirrors the reference's pybind11 module (proj/bindings/module.cpp:51-107):
+same function names, same argument meaning, and the same errors —
+``ValueError`` for an odd byte length (module.cpp:25-26) and for an unknown
+kernel name (module.cpp:45), ``RuntimeError`` for device/CUDA failures. The
+only route to compute is the C ABI; without the built library this module
+raises ImportError (no eager/CPU fallback exists).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libu16m.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"{_LIB_PATH} is missing: build it with `python paper_2601_06349_b200/_build.py` "
+        "(or __graft_entry__.build()). There is no CPU fallback.")
+
+_L = ctypes.CDLL(_LIB_PATH)
+_u16p = ctypes.c_void_p
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+_st = ctypes.c_int
+
+_L.u16m_to_well_formed.argtypes = [_u16p, _sz, _u16p, _vp]
+_L.u16m_to_well_formed_in_place.argtypes = [_u16p, _sz, _vp]
+_L.u16m_to_well_formed_batched.argtypes = [_u16p, _vp, _sz, _u16p, _vp]
+_L.u16m_to_well_formed_halo.argtypes = [_u16p, _sz, _u16p, ctypes.c_int32, ctypes.c_int32, _vp]
+_L.u16m_to_well_formed_halo_ptr.argtypes = [_u16p, _sz, _u16p, _vp, _vp, _vp]
+_L.u16m_to_well_formed_sharded.argtypes = [ctypes.c_int, _vp, _vp, _vp, _vp]
+_L.u16m_to_well_formed_host.argtypes = [_u16p, _sz, _u16p]
+_L.u16m_count_unpaired.argtypes = [_u16p, _sz, _vp, _vp]
+_L.u16m_unpaired_offsets.argtypes = [_u16p, _sz, _sz, _vp, _vp, _vp]
+_L.u16m_status_string.argtypes = [_st]
+_L.u16m_status_string.restype = ctypes.c_char_p
+_L.u16m_last_error.restype = ctypes.c_char_p
+_L.u16m_api_version.restype = ctypes.c_int
+_L.u16m_launch_count.restype = ctypes.c_ulonglong
+_L.u16m_gen_config.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                               ctypes.c_uint64, ctypes.c_uint64, _u16p, _vp]
+_L.u16m_gen_c3_offsets.argtypes = [ctypes.c_uint64, _sz, _vp, ctypes.POINTER(ctypes.c_uint64)]
+_L.u16m_gen_c3_content.argtypes = [ctypes.c_uint64, _sz, _vp, _u16p, _vp]
+_L.u16m_generate_reference_mix.argtypes = [_sz, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, _u16p]
+_L.u16m_l2_flush.argtypes = [_vp, _sz, _vp]
+for _f in ("u16m_to_well_formed", "u16m_to_well_formed_in_place", "u16m_to_well_formed_batched",
+           "u16m_to_well_formed_halo", "u16m_to_well_formed_halo_ptr", "u16m_to_well_formed_sharded",
+           "u16m_to_well_formed_host", "u16m_count_unpaired", "u16m_unpaired_offsets",
+           "u16m_gen_config", "u16m_gen_c3_offsets", "u16m_gen_c3_content",
+           "u16m_generate_reference_mix", "u16m_l2_flush"):
+    getattr(_L, _f).restype = _st
+
+OK, INVALID, ALIAS, NOT_DEVICE, CUDA, MISALIGNED, NO_DEVICE = range(7)
+
+# Reference kernel names (proj/src/driver.cpp:25-37) are accepted for source
+# compatibility and all served by the one sm_100a path.
+_KERNEL_NAMES = {"scalar", "generic", "generic4", "generic8", "generic16", "generic32", "bitmask",
+                 "bitmask-emulated", "bytesplit", "bytesplit-emulated", "cuda", "cuda-sm100a"}
+
+
+class U16MError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        super().__init__(f"{_L.u16m_status_string(status).decode()}: {detail}")
+
+
+def _check(st: int) -> None:
+    if st == OK:
+        return
+    detail = (_L.u16m_last_error() or b"").decode()
+    msg = f"{_L.u16m_status_string(st).decode()}: {detail}"
+    if st in (INVALID, ALIAS, MISALIGNED, NOT_DEVICE):
+        raise ValueError(msg)
+    raise U16MError(st, detail)
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def api_version() -> int:
+    return int(_L.u16m_api_version())
+
+
+def launch_count() -> int:
+    return int(_L.u16m_launch_count())
+
+
+def raw():
+    """The ctypes handle (bench / tests)."""
+    return _L
+
+
+# ---- device tensor API -------------------------------------------------------
+def _units(t: torch.Tensor, name: str) -> torch.Tensor:
+    if t.dtype not in (torch.int16, torch.uint16):
+        raise ValueError(f"{name} must be an int16/uint16 tensor of UTF-16 code units")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (use fix_utf16le for host bytes)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _stream(t: torch.Tensor, stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream(t.device).cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def to_well_formed(x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """out = repair(x) on the GPU (reference to_well_formed, driver.hpp:64-65)."""
+    _units(x, "x")
+    if out is None:
+        out = torch.empty_like(x)
+    _units(out, "out")
+    if out.numel() != x.numel():
+        raise ValueError("to_well_formed: input and output lengths differ")
+    with torch.cuda.device(x.device):
+        _check(_L.u16m_to_well_formed(x.data_ptr(), x.numel(), out.data_ptr(), _stream(x, stream)))
+    return out
+
+
+def to_well_formed_(x: torch.Tensor, stream=None) -> torch.Tensor:
+    """In-place repair (reference to_well_formed_in_place, driver.hpp:68-69)."""
+    _units(x, "x")
+    with torch.cuda.device(x.device):
+        _check(_L.u16m_to_well_formed_in_place(x.data_ptr(), x.numel(), _stream(x, stream)))
+    return x
+
+
+def to_well_formed_halo(x: torch.Tensor, out: Optional[torch.Tensor], left: int, right: int,
+                        stream=None) -> torch.Tensor:
+    """Repair one contiguous shard of a larger logical buffer; left/right are the
+    neighbouring units (-1 at the logical buffer's ends). out=None: in place."""
+    _units(x, "x")
+    out = x if out is None else _units(out, "out")
+    with torch.cuda.device(x.device):
+        _check(_L.u16m_to_well_formed_halo(x.data_ptr(), x.numel(), out.data_ptr(), int(left), int(right),
+                                           _stream(x, stream)))
+    return out
+
+
+def to_well_formed_batched(data: torch.Tensor, offsets: torch.Tensor, out: Optional[torch.Tensor] = None,
+                           stream=None) -> torch.Tensor:
+    """Repair every string [offsets[s], offsets[s+1]) independently."""
+    _units(data, "data")
+    if offsets.dtype != torch.int64 or not offsets.is_cuda or not offsets.is_contiguous():
+        raise ValueError("offsets must be a contiguous int64 CUDA tensor")
+    if offsets.numel() < 1:
+        raise ValueError("offsets must have num_strings + 1 entries")
+    if out is None:
+        out = data.clone()
+    _units(out, "out")
+    with torch.cuda.device(data.device):
+        _check(_L.u16m_to_well_formed_batched(data.data_ptr(), offsets.data_ptr(), offsets.numel() - 1,
+                                              out.data_ptr(), _stream(data, stream)))
+    return out
+
+
+def to_well_formed_sharded(shards: Sequence[torch.Tensor], outs: Optional[Sequence[torch.Tensor]] = None):
+    """One logical buffer = concatenation of `shards` (any CUDA devices of this
+    process). outs=None: in place. Synchronous."""
+    shards = [_units(s, "shard") for s in shards]
+    outs = shards if outs is None else [_units(o, "out") for o in outs]
+    n = len(shards)
+    if len(outs) != n or any(o.numel() != s.numel() for o, s in zip(outs, shards)):
+        raise ValueError("outs must match shards")
+    for s in shards:
+        torch.cuda.current_stream(s.device).synchronize()
+    dev = (ctypes.c_int * n)(*[s.device.index for s in shards])
+    ins = (ctypes.c_void_p * n)(*[s.data_ptr() for s in shards])
+    lens = (ctypes.c_size_t * n)(*[s.numel() for s in shards])
+    ous = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
+    _check(_L.u16m_to_well_formed_sharded(n, ctypes.addressof(dev), ctypes.addressof(ins),
+                                          ctypes.addressof(lens), ctypes.addressof(ous)))
+    return list(outs)
+
+
+def count_unpaired(x: torch.Tensor, stream=None) -> int:
+    """Number of units repair would rewrite (0 <=> well-formed). Synchronises."""
+    _units(x, "x")
+    cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
+    with torch.cuda.device(x.device):
+        _check(_L.u16m_count_unpaired(x.data_ptr(), x.numel(), cnt.data_ptr(), _stream(x, stream)))
+    return int(cnt.item())
+
+
+def unpaired_offsets_device(x: torch.Tensor, limit: Optional[int] = None, stream=None) -> torch.Tensor:
+    """Ascending offsets (int64 CUDA tensor) of the units repair would rewrite."""
+    _units(x, "x")
+    cap = x.numel() if limit is None else max(0, min(int(limit), x.numel()))
+    offs = torch.empty(max(cap, 1), dtype=torch.int64, device=x.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
+    with torch.cuda.device(x.device):
+        _check(_L.u16m_unpaired_offsets(x.data_ptr(), x.numel(), cap, offs.data_ptr(), cnt.data_ptr(),
+                                        _stream(x, stream)))
+    return offs[: int(cnt.item())]
+
+
+# ---- reference-compatible bytes API (proj/bindings/module.cpp) ---------------
+def _kernel_from_name(kernel: Optional[str]) -> None:
+    if kernel is not None and kernel not in _KERNEL_NAMES:
+        raise ValueError(f"unknown kernel '{kernel}'")
+
+
+def _check_bytes(data) -> memoryview:
+    mv = memoryview(data).cast("B")
+    if mv.nbytes % 2 != 0:
+        raise ValueError("UTF-16 byte string must have an even length")
+    return mv
+
+
+def _device_units(data) -> torch.Tensor:
+    mv = _check_bytes(data)
+    if mv.nbytes == 0:
+        return torch.empty(0, dtype=torch.int16, device="cuda")
+    host = torch.frombuffer(bytearray(mv), dtype=torch.int16)
+    return host.to("cuda", non_blocking=False)
+
+
+def fix_utf16le(data, kernel: Optional[str] = None) -> bytes:
+    """Return `data` (raw UTF-16LE code units) with every unpaired surrogate
+    replaced by U+FFFD (module.cpp:54-64). Host memory is staged through the
+    GPU by u16m_to_well_formed_host."""
+    mv = _check_bytes(data)
+    _kernel_from_name(kernel)
+    n = mv.nbytes // 2
+    out = bytearray(mv.nbytes)
+    if n == 0:
+        return bytes(out)
+    src = bytearray(mv) if mv.readonly else mv
+    in_buf = (ctypes.c_char * mv.nbytes).from_buffer(src)
+    out_buf = (ctypes.c_char * mv.nbytes).from_buffer(out)
+    _check(_L.u16m_to_well_formed_host(ctypes.addressof(in_buf), n, ctypes.addressof(out_buf)))
+    return bytes(out)
+
+
+def fix_str(text: str, kernel: Optional[str] = None) -> str:
+    """Return `text` with every unpaired surrogate replaced by U+FFFD
+    (proj/python/utf16mend/__init__.py:24-31)."""
+    data = text.encode("utf-16-le", "surrogatepass")
+    return fix_utf16le(data, kernel).decode("utf-16-le")
+
+
+def is_well_formed_utf16le(data) -> bool:
+    """True if `data` contains no unpaired surrogate (module.cpp:66-70)."""
+    t = _device_units(data)
+    return t.numel() == 0 or count_unpaired(t) == 0
+
+
+def is_well_formed_str(text: str) -> bool:
+    return is_well_formed_utf16le(text.encode("utf-16-le", "surrogatepass"))
+
+
+def unpaired_surrogate_offsets(data, limit: int = 2**64 - 1) -> list[int]:
+    """Unit offsets that fixing would rewrite, capped at `limit` (module.cpp:72-78)."""
+    t = _device_units(data)
+    if t.numel() == 0 or limit == 0:
+        return []
+    return [int(v) for v in unpaired_offsets_device(t, min(limit, t.numel())).cpu().tolist()]
+
+
+def generate_utf16le(units: int, pair_pct: float = 0.0, mismatch_pct: float = 0.0, seed: int = 0) -> bytes:
+    """Deterministic random UTF-16LE (the reference's generate(),
+    proj/src/datagen.cpp:44-74, via module.cpp:80-93)."""
+    if not (0.0 <= pair_pct <= 1.0 and 0.0 <= mismatch_pct <= 1.0):
+        raise ValueError("pair_pct and mismatch_pct must be within [0, 1]")
+    out = bytearray(2 * units)
+    if units == 0:
+        return bytes(out)
+    buf = (ctypes.c_char * len(out)).from_buffer(out)
+    _check(_L.u16m_generate_reference_mix(units, pair_pct, mismatch_pct, seed, ctypes.addressof(buf)))
+    return bytes(out)
+
+
+def available_kernels() -> list[str]:
+    """Names of every repair kernel selectable on this host (module.cpp:95-102)."""
+    return ["cuda-sm100a"]
+
+
+def default_kernel() -> str:
+    return "cuda-sm100a"
+
+
+# ---- device datagen (bench / tests) -----------------------------------------
+def gen_config(cfg: int, total: int, seed: Optional[int] = None, first: int = 0, count: Optional[int] = None,
+               shard_len: int = 0, out: Optional[torch.Tensor] = None, device="cuda", stream=None) -> torch.Tensor:
+    seed = cfg if seed is None else seed
+    count = total - first if count is None else count
+    if out is None:
+        out = torch.empty(count, dtype=torch.int16, device=device)
+    with torch.cuda.device(out.device):
+        _check(_L.u16m_gen_config(cfg, seed, total, shard_len, first, count, out.data_ptr(), _stream(out, stream)))
+    return out
+
+
+def gen_c3(num_strings: int, seed: int = 3, device="cuda") -> tuple[torch.Tensor, torch.Tensor]:
+    offsets = torch.empty(num_strings + 1, dtype=torch.int64, device=device)
+    total = ctypes.c_uint64(0)
+    with torch.cuda.device(offsets.device):
+        torch.cuda.current_stream().synchronize()
+        _check(_L.u16m_gen_c3_offsets(seed, num_strings, offsets.data_ptr(), ctypes.byref(total)))
+        data = torch.empty(int(total.value), dtype=torch.int16, device=device)
+        _check(_L.u16m_gen_c3_content(seed, num_strings, offsets.data_ptr(), data.data_ptr(),
+                                      _stream(data, None)))
+    return data, offsets
+
+
+def l2_flush(buf: torch.Tensor, stream=None) -> None:
+    _check(_L.u16m_l2_flush(buf.data_ptr(), buf.numel() * buf.element_size(), _stream(buf, stream)))

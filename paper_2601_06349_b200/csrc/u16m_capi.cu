@@ -1,0 +1,337 @@
+// C ABI (include/u16m.h): argument validation, stream plumbing, the host
+// staging pipeline and the multi-GPU shard driver. All compute goes through
+// the sm_100a kernels in u16m_kernels.cu — there is no CPU fallback.
+//
+// Error behaviour mirrors the reference boundary (proj/src/driver.cpp:135-142):
+// a length/argument problem is U16M_ERR_INVALID_ARGUMENT (the reference
+// throws std::invalid_argument), a partial in/out overlap is U16M_ERR_ALIAS
+// (the reference asserts), and hardware problems are U16M_ERR_CUDA /
+// U16M_ERR_NO_DEVICE (the reference throws std::runtime_error when a native
+// backend is missing, proj/src/bitmask_kernel.cpp:102-104).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/u16m.h"
+#include "u16m_internal.h"
+
+namespace {
+
+thread_local std::string t_last_error;
+
+u16m_status fail(u16m_status st, const std::string& detail) {
+  t_last_error = detail;
+  return st;
+}
+
+u16m_status cuda_fail(cudaError_t e, const char* what) {
+  std::string d = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return fail(U16M_ERR_CUDA, d);
+}
+
+u16m_status check_device_present() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(U16M_ERR_NO_DEVICE, "no CUDA device visible (u16m has no CPU fallback)");
+  }
+  return U16M_OK;
+}
+
+// Device-accessible: device or managed memory, or pinned host memory mapped
+// into the device address space.
+u16m_status check_device_ptr(const void* p, const char* name) {
+  cudaPointerAttributes a;
+  const cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(U16M_ERR_NOT_DEVICE_MEMORY, std::string(name) + " is not a CUDA-visible pointer");
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return U16M_OK;
+  if (a.type == cudaMemoryTypeHost && a.devicePointer != nullptr) return U16M_OK;
+  return fail(U16M_ERR_NOT_DEVICE_MEMORY,
+              std::string(name) + " is host memory; use u16m_to_well_formed_host or the C++ API");
+}
+
+u16m_status check_pair(const uint16_t* in, size_t n, const uint16_t* out) {
+  if (n == 0) return U16M_OK;
+  if (in == nullptr || out == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "null buffer with n > 0");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 1u)
+    return fail(U16M_ERR_MISALIGNED, "UTF-16 buffers must be 2-byte aligned");
+  if (in != out && in < out + n && out < in + n)
+    return fail(U16M_ERR_ALIAS, "in and out overlap partially (must be equal or disjoint)");
+  return U16M_OK;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+#define U16M_TRY(expr)                 \
+  do {                                 \
+    const u16m_status _st = (expr);    \
+    if (_st != U16M_OK) return _st;    \
+  } while (0)
+
+// ---- host staging pipeline -------------------------------------------------
+constexpr int kPipeStreams = 4;
+constexpr size_t kChunkUnits = size_t(8) << 20;  // 16 MiB per chunk
+
+struct HostPipe {
+  int device = -1;
+  cudaStream_t streams[kPipeStreams] = {};
+  uint16_t* dbuf[kPipeStreams] = {};
+};
+
+std::mutex g_pipe_mu;
+std::vector<HostPipe*> g_pipes;  // one per device, created lazily, never freed
+
+HostPipe* pipe_for(int device, u16m_status* st) {
+  for (HostPipe* p : g_pipes)
+    if (p->device == device) return p;
+  auto* p = new HostPipe;
+  p->device = device;
+  for (int i = 0; i < kPipeStreams; i++) {
+    cudaError_t e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&p->dbuf[i], kChunkUnits * sizeof(uint16_t));
+    if (e != cudaSuccess) {
+      *st = cuda_fail(e, "host pipeline setup");
+      return nullptr;
+    }
+  }
+  g_pipes.push_back(p);
+  return p;
+}
+
+// ---- shard driver state ------------------------------------------------------
+std::mutex g_peer_mu;
+std::vector<std::pair<int, int>> g_peer_enabled;
+
+bool ensure_peer(int from, int to) {
+  if (from == to) return true;
+  std::lock_guard<std::mutex> lock(g_peer_mu);
+  for (auto& pr : g_peer_enabled)
+    if (pr.first == from && pr.second == to) return true;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, from, to) != cudaSuccess || !can) {
+    cudaGetLastError();
+    return false;
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(from);
+  cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
+  cudaGetLastError();
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return false;
+  g_peer_enabled.emplace_back(from, to);
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* u16m_status_string(u16m_status status) {
+  switch (status) {
+    case U16M_OK: return "ok";
+    case U16M_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case U16M_ERR_ALIAS: return "in and out overlap partially";
+    case U16M_ERR_NOT_DEVICE_MEMORY: return "pointer is not device-accessible memory";
+    case U16M_ERR_CUDA: return "CUDA error";
+    case U16M_ERR_MISALIGNED: return "pointer is not 2-byte aligned";
+    case U16M_ERR_NO_DEVICE: return "no CUDA device";
+  }
+  return "unknown status";
+}
+
+const char* u16m_last_error(void) { return t_last_error.c_str(); }
+int u16m_api_version(void) { return U16M_API_VERSION; }
+unsigned long long u16m_launch_count(void) { return u16m::launch_count(); }
+
+u16m_status u16m_to_well_formed_halo_ptr(const uint16_t* in, size_t n, uint16_t* out,
+                                         const uint16_t* left_ptr, const uint16_t* right_ptr,
+                                         void* stream) {
+  U16M_TRY(check_pair(in, n, out));
+  if (n == 0) return U16M_OK;
+  U16M_TRY(check_device_present());
+  U16M_TRY(check_device_ptr(in, "in"));
+  if (out != in) U16M_TRY(check_device_ptr(out, "out"));
+  const cudaError_t e = u16m::launch_repair(in, n, out, -1, -1, left_ptr, right_ptr, as_stream(stream));
+  return e == cudaSuccess ? U16M_OK : cuda_fail(e, "repair kernel launch");
+}
+
+u16m_status u16m_to_well_formed_halo(const uint16_t* in, size_t n, uint16_t* out, int32_t left,
+                                     int32_t right, void* stream) {
+  if (left > 0xFFFF || right > 0xFFFF || left < -1 || right < -1)
+    return fail(U16M_ERR_INVALID_ARGUMENT, "halo values must be a code unit or -1");
+  U16M_TRY(check_pair(in, n, out));
+  if (n == 0) return U16M_OK;
+  U16M_TRY(check_device_present());
+  U16M_TRY(check_device_ptr(in, "in"));
+  if (out != in) U16M_TRY(check_device_ptr(out, "out"));
+  const cudaError_t e = u16m::launch_repair(in, n, out, left, right, nullptr, nullptr, as_stream(stream));
+  return e == cudaSuccess ? U16M_OK : cuda_fail(e, "repair kernel launch");
+}
+
+u16m_status u16m_to_well_formed(const uint16_t* in, size_t n, uint16_t* out, void* stream) {
+  return u16m_to_well_formed_halo(in, n, out, -1, -1, stream);
+}
+
+u16m_status u16m_to_well_formed_in_place(uint16_t* buf, size_t n, void* stream) {
+  return u16m_to_well_formed_halo(buf, n, buf, -1, -1, stream);
+}
+
+u16m_status u16m_to_well_formed_batched(const uint16_t* in, const int64_t* offsets,
+                                        size_t num_strings, uint16_t* out, void* stream) {
+  if (offsets == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "offsets is null");
+  if (num_strings == 0) return U16M_OK;
+  if (in == nullptr || out == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "null buffer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 1u)
+    return fail(U16M_ERR_MISALIGNED, "UTF-16 buffers must be 2-byte aligned");
+  if (reinterpret_cast<uintptr_t>(offsets) & 7u)
+    return fail(U16M_ERR_MISALIGNED, "offsets must be 8-byte aligned");
+  U16M_TRY(check_device_present());
+  U16M_TRY(check_device_ptr(in, "in"));
+  if (out != in) U16M_TRY(check_device_ptr(out, "out"));
+  U16M_TRY(check_device_ptr(offsets, "offsets"));
+  const cudaError_t e = u16m::launch_batched(in, offsets, num_strings, out, as_stream(stream));
+  return e == cudaSuccess ? U16M_OK : cuda_fail(e, "batched repair kernel launch");
+}
+
+u16m_status u16m_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
+                                void* stream) {
+  if (count_out == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "count_out is null");
+  if (n > 0 && in == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "null buffer with n > 0");
+  if (reinterpret_cast<uintptr_t>(in) & 1u) return fail(U16M_ERR_MISALIGNED, "in not 2-byte aligned");
+  U16M_TRY(check_device_present());
+  U16M_TRY(check_device_ptr(count_out, "count_out"));
+  if (n > 0) U16M_TRY(check_device_ptr(in, "in"));
+  const cudaError_t e = u16m::launch_count_unpaired(in, n, count_out, as_stream(stream));
+  return e == cudaSuccess ? U16M_OK : cuda_fail(e, "count kernel launch");
+}
+
+u16m_status u16m_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
+                                  unsigned long long* offsets_out, unsigned long long* count_out,
+                                  void* stream) {
+  if (count_out == nullptr || (limit > 0 && offsets_out == nullptr))
+    return fail(U16M_ERR_INVALID_ARGUMENT, "null output");
+  if (n > 0 && in == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "null buffer with n > 0");
+  if (reinterpret_cast<uintptr_t>(in) & 1u) return fail(U16M_ERR_MISALIGNED, "in not 2-byte aligned");
+  U16M_TRY(check_device_present());
+  U16M_TRY(check_device_ptr(count_out, "count_out"));
+  if (limit > 0) U16M_TRY(check_device_ptr(offsets_out, "offsets_out"));
+  if (n > 0) U16M_TRY(check_device_ptr(in, "in"));
+  const cudaError_t e =
+      u16m::launch_unpaired_offsets(in, n, limit, offsets_out, count_out, as_stream(stream));
+  return e == cudaSuccess ? U16M_OK : cuda_fail(e, "offsets kernels");
+}
+
+u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out) {
+  U16M_TRY(check_pair(in, n, out));
+  if (n == 0) return U16M_OK;
+  U16M_TRY(check_device_present());
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(g_pipe_mu);  // one staged job per process at a time
+  u16m_status st = U16M_OK;
+  HostPipe* p = pipe_for(dev, &st);
+  if (p == nullptr) return st;
+  size_t c = 0;
+  for (size_t c0 = 0; c0 < n; c0 += kChunkUnits, c++) {
+    const size_t len = std::min(kChunkUnits, n - c0);
+    const int k = static_cast<int>(c % kPipeStreams);
+    cudaStream_t s = p->streams[k];
+    // Halo units are read from the host copy at enqueue time. For in-place
+    // jobs an earlier chunk's D2H may already have rewritten in[c0-1]; that
+    // is benign (a unit is only rewritten when no neighbour pairs with it).
+    const int32_t left = c0 > 0 ? static_cast<int32_t>(in[c0 - 1]) : -1;
+    const int32_t right = c0 + len < n ? static_cast<int32_t>(in[c0 + len]) : -1;
+    e = cudaMemcpyAsync(p->dbuf[k], in + c0, len * 2, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, s);
+    if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
+    e = cudaMemcpyAsync(out + c0, p->dbuf[k], len * 2, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  }
+  for (int k = 0; k < kPipeStreams; k++) {
+    e = cudaStreamSynchronize(p->streams[k]);
+    if (e != cudaSuccess) return cuda_fail(e, "host pipeline sync");
+  }
+  return U16M_OK;
+}
+
+u16m_status u16m_to_well_formed_sharded(int num_shards, const int* device_ids,
+                                        const uint16_t* const* shard_in, const size_t* shard_len,
+                                        uint16_t* const* shard_out) {
+  if (num_shards < 0 || (num_shards > 0 && (!device_ids || !shard_in || !shard_len || !shard_out)))
+    return fail(U16M_ERR_INVALID_ARGUMENT, "null shard table");
+  if (num_shards == 0) return U16M_OK;
+  U16M_TRY(check_device_present());
+  int prev = 0;
+  cudaGetDevice(&prev);
+  for (int g = 0; g < num_shards; g++) {
+    U16M_TRY(check_pair(shard_in[g], shard_len[g], shard_out[g]));
+    if (shard_len[g] == 0) continue;
+    if (cudaSetDevice(device_ids[g]) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(U16M_ERR_INVALID_ARGUMENT, "bad device id");
+    }
+    U16M_TRY(check_device_ptr(shard_in[g], "shard_in"));
+    if (shard_out[g] != shard_in[g]) U16M_TRY(check_device_ptr(shard_out[g], "shard_out"));
+  }
+  // Halo pointers: the last unit of the previous non-empty shard and the first
+  // unit of the next one, read by the kernel directly (same device, or a peer
+  // over NVLink). Without peer access the unit is fetched by value.
+  std::vector<cudaStream_t> streams(num_shards, nullptr);
+  u16m_status st = U16M_OK;
+  for (int g = 0; g < num_shards && st == U16M_OK; g++) {
+    if (shard_len[g] == 0) continue;
+    const int dev = device_ids[g];
+    int lk = g - 1, rk = g + 1;
+    while (lk >= 0 && shard_len[lk] == 0) lk--;
+    while (rk < num_shards && shard_len[rk] == 0) rk++;
+    const uint16_t* lp = lk >= 0 ? shard_in[lk] + shard_len[lk] - 1 : nullptr;
+    const uint16_t* rp = rk < num_shards ? shard_in[rk] : nullptr;
+    int32_t lv = -1, rv = -1;
+    if (lp && !ensure_peer(dev, device_ids[lk])) {
+      uint16_t u = 0;
+      cudaSetDevice(device_ids[lk]);
+      cudaError_t e = cudaMemcpy(&u, lp, 2, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) { st = cuda_fail(e, "halo fetch"); break; }
+      lv = u;
+      lp = nullptr;
+    }
+    if (rp && !ensure_peer(dev, device_ids[rk])) {
+      uint16_t u = 0;
+      cudaSetDevice(device_ids[rk]);
+      cudaError_t e = cudaMemcpy(&u, rp, 2, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) { st = cuda_fail(e, "halo fetch"); break; }
+      rv = u;
+      rp = nullptr;
+    }
+    cudaSetDevice(dev);
+    cudaError_t e = cudaStreamCreateWithFlags(&streams[g], cudaStreamNonBlocking);
+    if (e != cudaSuccess) { st = cuda_fail(e, "stream create"); break; }
+    e = u16m::launch_repair(shard_in[g], shard_len[g], shard_out[g], lv, rv, lp, rp, streams[g]);
+    if (e != cudaSuccess) { st = cuda_fail(e, "shard kernel launch"); break; }
+  }
+  for (int g = 0; g < num_shards; g++) {
+    if (!streams[g]) continue;
+    cudaSetDevice(device_ids[g]);
+    const cudaError_t e = cudaStreamSynchronize(streams[g]);
+    if (e != cudaSuccess && st == U16M_OK) st = cuda_fail(e, "shard sync");
+    cudaStreamDestroy(streams[g]);
+  }
+  cudaSetDevice(prev);
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,30 @@
+// Internal host-side declarations shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace u16m {
+
+// Repair [0,n) of `in` into `out` (out == in: in place). left/right: halo
+// unit values (-1 = outside); left_ptr/right_ptr: device-side halo units
+// (override the values when non-null).
+cudaError_t launch_repair(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
+                          const uint16_t* left_ptr, const uint16_t* right_ptr, cudaStream_t stream);
+
+cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
+                           uint16_t* out, cudaStream_t stream);
+
+cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
+                                  cudaStream_t stream);
+
+cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
+                                    unsigned long long* offsets_out, unsigned long long* count_out,
+                                    cudaStream_t stream);
+
+unsigned long long launch_count();
+void note_launch();
+
+}  // namespace u16m

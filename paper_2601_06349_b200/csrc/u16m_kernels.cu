@@ -1,0 +1,448 @@
+// sm_100a repair kernels: stream (copy / in-place / count) and batched CSR.
+//
+// One kernel template covers every form of the path. A CTA tile is 8 warps ×
+// 32 lanes × kVecs 16-byte vectors = 8192 contiguous units (16 KiB); each warp
+// owns 2 KiB of it. Per tile:
+//   1. every lane issues its kVecs 128-bit loads up front (64 B in flight per
+//      thread; at 2048 resident threads per SM that is 128 KiB per SM, well
+//      above the ~45 KiB/SM Little's-law requirement at 6.4 TB/s);
+//   2. lanes 0 and 31 load the 2-byte halo unit on each side of the warp tile
+//      (a line the neighbouring warp streams anyway, so it is an L2 hit);
+//   3. classification + warp-shuffle halo + blend entirely in registers
+//      (u16m_repair.cuh);
+//   4. one 128-bit streaming store per vector (copy), or a store only for
+//      vectors that contain a rewrite (in-place: clean vectors cost no write).
+//
+// In-place race: a neighbouring warp may read a halo
+// unit after its owner rewrote it to FFFD. A unit is only rewritten when no
+// neighbour pairs with it, so the reader's decision is the same for the old
+// and the new value; the 16-bit unit is read atomically either way.
+//
+// Batched form: units are the flat concatenation [offsets[0], offsets[S]);
+// per tile, warp 0 finds the first string start inside the tile with a
+// 32-ary warp-cooperative search over `offsets` (4 dependent rounds for 2^20
+// strings) and marks every string start in a shared-memory bitmap; the
+// stencil then treats a start as "no predecessor" and the unit before it as
+// "no successor". The search runs while the tile's data loads are in flight.
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+
+#include "u16m_internal.h"
+#include "u16m_repair.cuh"
+
+namespace u16m {
+
+enum Mode : int {
+  kCopy = 0,       // out = repair(in)
+  kInPlace = 1,    // buf = repair(buf), stores only vectors with a rewrite
+  kCount = 2,      // *count_out += number of units repair would rewrite
+  kTileCount = 3,  // tile_counts[tile] = rewrites in that CTA tile
+  kEmit = 4        // write ascending rewrite offsets (< limit) using tile prefixes
+};
+
+struct BatchArgs {
+  const int64_t* offsets;  // device, num_strings + 1 entries
+  uint64_t count;          // num_strings + 1
+  uint32_t phase;          // (in & 15) / 2
+};
+
+struct ScanArgs {
+  unsigned long long* count_out;    // kCount: total; kEmit: number written
+  uint32_t* tile_counts;            // kTileCount output
+  const unsigned long long* tile_prefix;  // kEmit input (exclusive prefix per tile)
+  unsigned long long* offsets_out;  // kEmit output
+  unsigned long long limit;         // kEmit cap
+};
+
+// First index in [0, count) with off[idx] >= key, or count. Warp-uniform.
+__device__ __forceinline__ uint64_t warp_lower_bound(const int64_t* off, uint64_t count, int64_t key,
+                                                     int lane) {
+  uint64_t lo = 0, hi = count;
+  while (hi - lo > 32) {
+    const uint64_t step = (hi - lo + 31) / 32;
+    const uint64_t idx = lo + static_cast<uint64_t>(lane) * step;
+    const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
+    const uint32_t m = __ballot_sync(kFull, pred);
+    if (m == 0) {
+      lo = lo + 31 * step + 1;
+    } else {
+      const int f = __ffs(m) - 1;
+      if (f == 0) {
+        hi = lo;
+      } else {
+        const uint64_t nlo = lo + static_cast<uint64_t>(f - 1) * step + 1;
+        const uint64_t cand = lo + static_cast<uint64_t>(f) * step;
+        hi = cand < hi ? cand : hi;
+        lo = nlo;
+      }
+    }
+  }
+  const uint64_t idx = lo + lane;
+  const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
+  const uint32_t m = __ballot_sync(kFull, pred);
+  return m ? lo + (__ffs(m) - 1) : hi;
+}
+
+// Clear the flags of units outside [lo, hi) (edge vectors only).
+__device__ __forceinline__ void mask_outside(const Span& s, uint64_t vi, uint32_t& B0, uint32_t& B1) {
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const uint64_t a = vi * 8 + j;
+    if (a < s.lo || a >= s.hi) {
+      if (j < 4) B0 &= ~(0x80u << (8 * j));
+      else B1 &= ~(0x80u << (8 * (j - 4)));
+    }
+  }
+}
+
+template <int kMode, bool kSamePhase, bool kBatched>
+__global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, ScanArgs sc) {
+  constexpr bool kScanMode = kMode == kTileCount || kMode == kEmit;
+  __shared__ uint32_t starts[kBatched ? (kCtaUnits / 32 + 2) : 1];
+  __shared__ unsigned long long warp_sums[kScanMode ? kWarps : 1];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+
+  if constexpr (kBatched) {
+    // Range of the batch, read on the device (no host sync in the API).
+    const int64_t A = __ldg(b.offsets);
+    const int64_t B = __ldg(b.offsets + b.count - 1);
+    s.lo = static_cast<uint64_t>(A) + b.phase;
+    s.hi = static_cast<uint64_t>(B) + b.phase;
+    s.out_units = reinterpret_cast<uint16_t*>(s.out) + s.lo;
+  }
+  if (s.hi <= s.lo) return;
+  const uint64_t vbeg = s.lo / 8;
+  const uint64_t vend = (s.hi + 7) / 8;
+  const uint64_t ntiles = (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
+  uint64_t counted = 0;
+
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t cta_v0 = vbeg + tile * kCtaVecs;
+    const uint64_t warp_v0 = cta_v0 + static_cast<uint64_t>(warp) * kWarpVecs;
+
+    uint4 v[kVecs];
+#pragma unroll
+    for (int k = 0; k < kVecs; k++) {
+      const uint64_t vi = warp_v0 + k * 32 + lane;
+      v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
+    }
+    uint32_t halo = 0;
+    if (lane == 0) halo = unit_at(s, static_cast<int64_t>(warp_v0 * 8) - 1);
+    if (lane == 31) halo = unit_at(s, static_cast<int64_t>((warp_v0 + kWarpVecs) * 8));
+
+    if constexpr (kBatched) {
+      __syncthreads();  // previous tile's readers are done with `starts`
+      if (warp == 0) {
+        for (int i = lane; i < kCtaUnits / 32 + 2; i += 32) starts[i] = 0;
+        __syncwarp();
+        const int64_t key_lo = static_cast<int64_t>(cta_v0 * 8) - static_cast<int64_t>(b.phase);
+        const int64_t key_hi = key_lo + kCtaUnits;
+        uint64_t sidx = warp_lower_bound(b.offsets, b.count, key_lo, lane);
+        for (;;) {
+          const uint64_t idx = sidx + lane;
+          const int64_t p = idx < b.count ? __ldg(b.offsets + idx) : INT64_MAX;
+          const bool inside = p <= key_hi;
+          if (inside) {
+            const uint64_t bit = static_cast<uint64_t>(p - key_lo);
+            atomicOr(&starts[bit >> 5], 1u << (bit & 31));
+          }
+          if (__ballot_sync(kFull, inside) != kFull) break;
+          sidx += 32;
+        }
+      }
+      __syncthreads();
+    }
+
+    Flags f[kVecs];
+    bool edge[kVecs];
+#pragma unroll
+    for (int k = 0; k < kVecs; k++) {
+      const uint64_t vi = warp_v0 + k * 32 + lane;
+      edge[k] = vi * 8 < s.lo || vi * 8 + 8 > s.hi;
+      if (edge[k]) patch_edges(s, vi, v[k]);
+      f[k] = classify8(v[k]);
+    }
+    const uint32_t halo_h = hflag_hi(halo);
+    const uint32_t halo_l = lflag_lo(halo);
+    uint32_t up[kVecs], dn[kVecs];
+#pragma unroll
+    for (int k = 0; k < kVecs; k++) {
+      up[k] = __shfl_sync(kFull, f[k].H1, (lane + 31) & 31);
+      dn[k] = __shfl_sync(kFull, f[k].L0, (lane + 1) & 31);
+    }
+
+    uint32_t B0[kVecs], B1[kVecs];
+#pragma unroll
+    for (int k = 0; k < kVecs; k++) {
+      const uint64_t vi = warp_v0 + k * 32 + lane;
+      const uint32_t hp = lane ? up[k] : (k ? up[k - 1] : halo_h);
+      const uint32_t ln = lane != 31 ? dn[k] : (k + 1 < kVecs ? dn[k + 1] : halo_l);
+      if constexpr (kBatched) {
+        const uint32_t a0 = static_cast<uint32_t>((vi - cta_v0) * 8);
+        const uint64_t pair = static_cast<uint64_t>(starts[a0 >> 5]) |
+                              (static_cast<uint64_t>(starts[(a0 >> 5) + 1]) << 32);
+        const uint32_t bits = static_cast<uint32_t>(pair >> (a0 & 31));
+        bad8(f[k], hp, ln, B0[k], B1[k], spread4(bits), spread4(bits >> 4),
+             ((bits >> 8) & 1u) << 7);
+      } else {
+        bad8(f[k], hp, ln, B0[k], B1[k]);
+      }
+      if (kMode >= kCount && edge[k]) mask_outside(s, vi, B0[k], B1[k]);
+    }
+
+    if constexpr (kMode == kCopy || kMode == kInPlace) {
+#pragma unroll
+      for (int k = 0; k < kVecs; k++) {
+        const uint64_t vi = warp_v0 + k * 32 + lane;
+        if (vi >= vend) continue;
+        const bool dirty = (B0[k] | B1[k]) != 0;
+        if (kMode == kInPlace && !dirty) continue;
+        const uint4 r = blend(v[k], B0[k], B1[k]);
+        if (kSamePhase && !edge[k]) {
+          st_stream(s.out + vi, r);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const uint64_t a = vi * 8 + j;
+            if (a >= s.lo && a < s.hi) {
+              const uint32_t u = get_unit(r, j);
+              if (kMode == kCopy || u != get_unit(v[k], j))
+                s.out_units[a - s.lo] = static_cast<uint16_t>(u);
+            }
+          }
+        }
+      }
+    } else if constexpr (kMode == kCount) {
+#pragma unroll
+      for (int k = 0; k < kVecs; k++) counted += __popc(B0[k]) + __popc(B1[k]);
+    } else {
+      // Rank of each vector's rewrites inside the tile, in unit order
+      // (warp-major, then k, then lane).
+      uint32_t c[kVecs], pre[kVecs];
+      uint32_t warp_total = 0;
+#pragma unroll
+      for (int k = 0; k < kVecs; k++) {
+        c[k] = __popc(B0[k]) + __popc(B1[k]);
+        uint32_t x = c[k];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        pre[k] = warp_total + x - c[k];
+        warp_total += __shfl_sync(kFull, x, 31);
+      }
+      __syncthreads();  // previous tile's readers of warp_sums are done
+      if (lane == 0) warp_sums[warp] = warp_total;
+      __syncthreads();
+      unsigned long long before = 0, tile_total = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; w++) {
+        if (w < warp) before += warp_sums[w];
+        tile_total += warp_sums[w];
+      }
+      if constexpr (kMode == kTileCount) {
+        if (threadIdx.x == 0) sc.tile_counts[tile] = static_cast<uint32_t>(tile_total);
+      } else {
+        const unsigned long long base = sc.tile_prefix[tile] + before;
+        if (base < sc.limit) {
+#pragma unroll
+          for (int k = 0; k < kVecs; k++) {
+            unsigned long long r = base + pre[k];
+            const uint64_t vi = warp_v0 + k * 32 + lane;
+            uint64_t bits = static_cast<uint64_t>(B0[k]) | (static_cast<uint64_t>(B1[k]) << 32);
+            while (bits && r < sc.limit) {
+              const int bit = __ffsll(static_cast<long long>(bits)) - 1;
+              bits &= bits - 1;
+              const uint64_t a = vi * 8 + (bit >> 3);
+              sc.offsets_out[r++] = a - s.lo;
+            }
+          }
+        }
+        if (tile + 1 == ntiles && threadIdx.x == 0) {
+          const unsigned long long all = sc.tile_prefix[tile] + tile_total;
+          *sc.count_out = all < sc.limit ? all : sc.limit;
+        }
+      }
+    }
+  }
+
+  if constexpr (kMode == kCount) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) counted += __shfl_xor_sync(kFull, counted, o);
+    if (lane == 0 && counted) atomicAdd(sc.count_out, static_cast<unsigned long long>(counted));
+  }
+}
+
+// ---- host launchers --------------------------------------------------------
+
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+
+int sm_count_for_current_device() {
+  static std::mutex mu;
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cached[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+template <int kMode, bool kSamePhase, bool kBatched>
+cudaError_t launch(const Span& s, const BatchArgs& b, const ScanArgs& sc, uint64_t grid,
+                   cudaStream_t stream) {
+  if (grid == 0) return cudaSuccess;
+  if (grid > 0x7FFFFFFFull) grid = 0x7FFFFFFFull;
+  repair_kernel<kMode, kSamePhase, kBatched>
+      <<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(s, b, sc);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+constexpr BatchArgs kNoBatch{nullptr, 0, 0};
+constexpr ScanArgs kNoScan{nullptr, nullptr, nullptr, nullptr, 0};
+
+Span make_span(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
+               const uint16_t* left_ptr, const uint16_t* right_ptr, bool* same_phase) {
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
+  const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
+  Span s;
+  s.in = reinterpret_cast<const uint4*>(ia - 2 * ph);
+  s.out = reinterpret_cast<uint4*>(oa - 2 * ph);  // aligned only when same phase
+  s.out_units = out;
+  s.lo = ph;
+  s.hi = ph + n;
+  s.left = left;
+  s.right = right;
+  s.left_ptr = left_ptr;
+  s.right_ptr = right_ptr;
+  *same_phase = out != nullptr && ((ia & 15u) == (oa & 15u));
+  return s;
+}
+
+uint64_t tiles_for(const Span& s) {
+  const uint64_t vbeg = s.lo / 8, vend = (s.hi + 7) / 8;
+  return (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
+}
+}  // namespace
+
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+cudaError_t launch_repair(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
+                          const uint16_t* left_ptr, const uint16_t* right_ptr, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  bool same = false;
+  const Span s = make_span(in, n, out, left, right, left_ptr, right_ptr, &same);
+  const uint64_t grid = tiles_for(s);
+  if (in == out) return launch<kInPlace, true, false>(s, kNoBatch, kNoScan, grid, stream);
+  if (same) return launch<kCopy, true, false>(s, kNoBatch, kNoScan, grid, stream);
+  return launch<kCopy, false, false>(s, kNoBatch, kNoScan, grid, stream);
+}
+
+cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
+                                  cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(count_out, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess || n == 0) return e;
+  bool same = false;
+  const Span s = make_span(in, n, nullptr, -1, -1, nullptr, nullptr, &same);
+  ScanArgs sc = kNoScan;
+  sc.count_out = count_out;
+  const uint64_t tiles = tiles_for(s);
+  const uint64_t cap = static_cast<uint64_t>(sm_count_for_current_device()) * 8;
+  return launch<kCount, true, false>(s, kNoBatch, sc, tiles < cap ? tiles : cap, stream);
+}
+
+// Exclusive prefix over per-tile counts, one CTA, sequential chunks of 1024.
+__global__ void __launch_bounds__(1024) tile_prefix_kernel(const uint32_t* counts, uint64_t n,
+                                                           unsigned long long* prefix) {
+  __shared__ unsigned long long warp_tot[32];
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t base = 0; base < n; base += 1024) {
+    const uint64_t i = base + threadIdx.x;
+    const unsigned long long c = i < n ? counts[i] : 0;
+    unsigned long long x = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    unsigned long long before = carry;
+    for (int w = 0; w < warp; w++) before += warp_tot[w];
+    if (i < n) prefix[i] = before + x - c;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = before + x;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
+                                    unsigned long long* offsets_out, unsigned long long* count_out,
+                                    cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(count_out, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess || n == 0 || limit == 0) return e;
+  bool same = false;
+  const Span s = make_span(in, n, nullptr, -1, -1, nullptr, nullptr, &same);
+  const uint64_t tiles = tiles_for(s);
+  void* ws = nullptr;
+  e = cudaMallocAsync(&ws, tiles * (sizeof(uint32_t) + sizeof(unsigned long long)) + 16, stream);
+  if (e != cudaSuccess) return e;
+  auto* prefix = static_cast<unsigned long long*>(ws);
+  auto* counts = reinterpret_cast<uint32_t*>(prefix + tiles);
+  ScanArgs sc = kNoScan;
+  sc.tile_counts = counts;
+  e = launch<kTileCount, true, false>(s, kNoBatch, sc, tiles, stream);
+  if (e == cudaSuccess) {
+    tile_prefix_kernel<<<1, 1024, 0, stream>>>(counts, tiles, prefix);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    sc = kNoScan;
+    sc.count_out = count_out;
+    sc.tile_prefix = prefix;
+    sc.offsets_out = offsets_out;
+    sc.limit = limit;
+    e = launch<kEmit, true, false>(s, kNoBatch, sc, tiles, stream);
+  }
+  const cudaError_t f = cudaFreeAsync(ws, stream);
+  return e != cudaSuccess ? e : f;
+}
+
+cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
+                           uint16_t* out, cudaStream_t stream) {
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
+  const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
+  Span s;
+  s.in = reinterpret_cast<const uint4*>(ia - 2 * ph);
+  s.out = reinterpret_cast<uint4*>(oa - 2 * ph);
+  s.out_units = nullptr;  // set on the device from offsets[0]
+  s.lo = s.hi = 0;
+  s.left = s.right = -1;
+  s.left_ptr = s.right_ptr = nullptr;
+  const BatchArgs b{offsets, static_cast<uint64_t>(num_strings) + 1, ph};
+  // Persistent grid: the range is only known on the device.
+  const uint64_t grid = static_cast<uint64_t>(sm_count_for_current_device()) * 8;
+  const bool same = (ia & 15u) == (oa & 15u);
+  if (in == out) return launch<kInPlace, true, true>(s, b, kNoScan, grid, stream);
+  if (same) return launch<kCopy, true, true>(s, b, kNoScan, grid, stream);
+  return launch<kCopy, false, true>(s, b, kNoScan, grid, stream);
+}
+
+}  // namespace u16m

@@ -1,0 +1,104 @@
+"""One-process-per-GPU sharding of one logical UTF-16 buffer (north star item 5).
+
+The stencil needs exactly one unit on each side of a contiguous shard
+(SURVEY.md §8e), so the only exchange step is 2 units per rank: every rank
+contributes (first unit, last unit) of its shard to one tiny all-gather, and
+the repair kernel reads its neighbours' units straight from the gathered
+device tensor (u16m_to_well_formed_halo_ptr) — no host synchronisation inside
+a step. Ordering is not required even in place: a neighbour's edge unit
+yields the same decision whether it was read before or after that neighbour
+rewrote it.
+
+Host-side logic only; the compute call is injected so the same code runs with
+NCCL + the sm_100a kernel (bench.py) and with gloo + the CPU oracle
+(tests/test_dist_gloo.py).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+EMPTY = -1  # sentinel for an empty shard's edge
+
+
+def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, as-equal-as-possible shard [start, end) of rank."""
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def edge_tensor(shard: torch.Tensor) -> torch.Tensor:
+    """int32 [first, last] of a shard of int16/uint16 units (EMPTY if empty)."""
+    if shard.numel() == 0:
+        return torch.full((2,), EMPTY, dtype=torch.int32, device=shard.device)
+    u = shard.view(torch.int16)
+    return torch.stack([u[0], u[-1]]).to(torch.int32) & 0xFFFF
+
+
+def gather_edges(shard: torch.Tensor, group=None, device: Optional[torch.device] = None) -> torch.Tensor:
+    """[world, 2] int32 tensor of every rank's (first, last) unit."""
+    world = dist.get_world_size(group)
+    e = edge_tensor(shard)
+    if device is not None:
+        e = e.to(device)
+    out = torch.empty((world, 2), dtype=torch.int32, device=e.device)
+    dist.all_gather_into_tensor(out, e, group=group)
+    return out
+
+
+def halos_from_edges(edges: torch.Tensor, rank: int) -> tuple[int, int]:
+    """(left, right) neighbour units for `rank`, skipping empty shards; -1 at
+    the logical buffer's ends. Host values (synchronises if on device)."""
+    e = edges.cpu().tolist()
+    left = right = -1
+    for r in range(rank - 1, -1, -1):
+        if e[r][1] != EMPTY:
+            left = e[r][1]
+            break
+    for r in range(rank + 1, len(e)):
+        if e[r][0] != EMPTY:
+            right = e[r][0]
+            break
+    return left, right
+
+
+def halo_pointers(edges: torch.Tensor, rank: int) -> tuple[int, int]:
+    """Device addresses of the neighbours' edge units inside the gathered
+    int32 edges tensor (the low 16 bits of each little-endian int32 are the
+    unit), 0 for none. Requires every shard to be non-empty."""
+    world = edges.shape[0]
+    base = edges.data_ptr()
+    left = base + 4 * (2 * (rank - 1) + 1) if rank > 0 else 0
+    right = base + 4 * (2 * (rank + 1)) if rank + 1 < world else 0
+    return left, right
+
+
+def repair_shard(shard: torch.Tensor, out: Optional[torch.Tensor] = None, group=None, compute=None,
+                 all_nonempty: bool = True):
+    """Repair this rank's shard of the logical buffer.
+
+    Default: the sm_100a kernel through the C ABI, reading the neighbours'
+    units from the gathered device tensor (no host sync; requires every
+    rank's shard to be non-empty — pass all_nonempty=False otherwise).
+    `compute(shard, out, left, right)` replaces the kernel (CPU tests)."""
+    rank = dist.get_rank(group)
+    out = shard if out is None else out
+    edges = gather_edges(shard, group)
+    if compute is None and all_nonempty and shard.numel() > 0:
+        from . import _lib
+
+        lp, rp = halo_pointers(edges, rank)
+        st = _lib.raw().u16m_to_well_formed_halo_ptr(
+            shard.data_ptr(), shard.numel(), out.data_ptr(), lp or None, rp or None,
+            torch.cuda.current_stream(shard.device).cuda_stream)
+        _lib._check(st)
+        return out
+    left, right = halos_from_edges(edges, rank)
+    if compute is None:
+        from . import _lib
+
+        return _lib.to_well_formed_halo(shard, out, left, right)
+    return compute(shard, out, left, right)

@@ -1,0 +1,386 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle
+and the reference's golden vectors. Bit-exact everywhere (integer path)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from helpers import ALPHABET, boundary_sequences, concat_with_offsets, fuzz_inputs, sha
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint16).view(np.int16)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def gpu_copy(P, x):
+    return host(P.to_well_formed(dev(x)))
+
+
+def gpu_inplace(P, x):
+    t = dev(x)
+    P.to_well_formed_(t)
+    return host(t)
+
+
+def test_native_library_loaded(P, cuda):
+    import os
+
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert P.lib_path() in maps
+
+
+def test_mixed_sample_all_apis(P, cuda, golden):
+    _, arr = golden
+    x, e = arr["mixed_in"], arr["mixed_expected"]
+    assert (gpu_copy(P, x) == e).all()
+    assert (gpu_inplace(P, x) == e).all()
+    assert np.frombuffer(P.fix_utf16le(x.tobytes()), np.uint16).tolist() == e.tolist()
+    s = x.tobytes().decode("utf-16-le", "surrogatepass")
+    assert P.fix_str(s) == e.tobytes().decode("utf-16-le")
+    assert P.unpaired_surrogate_offsets(x.tobytes()) == [10, 21]
+    assert not P.is_well_formed_utf16le(x.tobytes())
+    assert P.is_well_formed_utf16le(e.tobytes())
+
+
+def test_scalar_examples(P, cuda, golden):
+    meta, _ = golden
+    for ex in meta["scalar_examples"]:
+        x = np.array(ex["in"], np.uint16)
+        if x.size == 0:
+            assert P.fix_utf16le(b"") == b""
+            continue
+        assert gpu_copy(P, x).tolist() == ex["out"]
+        assert gpu_inplace(P, x).tolist() == ex["out"]
+
+
+def test_boundary_exhaustive_individual(P, cuda, golden):
+    """Every boundary-alphabet sequence of length <= 3 as its own launch, plus
+    the stored length-4 golden outputs."""
+    _, arr = golden
+    for s in boundary_sequences(3):
+        if s.size == 0:
+            continue
+        e = O.fix_scalar(s)
+        assert (gpu_copy(P, s) == e).all()
+        assert (gpu_inplace(P, s) == e).all()
+
+
+def test_boundary4_and5_batched(P, cuda, golden):
+    meta, arr = golden
+    for L in (4, 5):
+        seqs = list(boundary_sequences(L))
+        data, offsets = concat_with_offsets(seqs)
+        assert sha(data) == meta[f"boundary{L}_sha_in"]
+        out = host(P.to_well_formed_batched(dev(data), torch.from_numpy(offsets).cuda()))
+        assert sha(out) == meta[f"boundary{L}_sha_out"]
+        if L == 4:
+            assert (out == arr["boundary4_out"]).all()
+        t = dev(data)
+        P.to_well_formed_batched(t, torch.from_numpy(offsets).cuda(), out=t)  # in place
+        assert sha(host(t)) == meta[f"boundary{L}_sha_out"]
+
+
+def test_generate_kats(P, cuda, golden):
+    meta, _ = golden
+    for k in meta["generate_kats"]:
+        x = np.frombuffer(P.generate_utf16le(k["n"], k["pair"], k["mismatch"], k["seed"]), np.uint16)
+        assert sha(x) == k["sha_in"]
+        assert sha(gpu_copy(P, x)) == k["sha_out"]
+        assert sha(gpu_inplace(P, x)) == k["sha_out"]
+        assert sha(np.frombuffer(P.fix_utf16le(x.tobytes()), np.uint16)) == k["sha_out"]
+        assert P.count_unpaired(dev(x)) == k["changed"]
+
+
+def test_fuzz_acceptance(P, cuda, golden):
+    meta, arr = golden
+    ins = fuzz_inputs(meta, arr, lambda n, p, m, s: np.frombuffer(P.generate_utf16le(n, p, m, s), np.uint16))
+    assert sha(np.concatenate(ins)) == meta["fuzz"]["sha_in"]
+    outs = [gpu_copy(P, x) if x.size else x for x in ins[:600]]
+    outs_ip = [gpu_inplace(P, x) if x.size else x for x in ins[:600]]
+    data, offsets = concat_with_offsets(ins)
+    batched = host(P.to_well_formed_batched(dev(data), torch.from_numpy(offsets).cuda()))
+    assert sha(batched) == meta["fuzz"]["sha_out"]
+    assert (np.concatenate(outs) == batched[: offsets[600]]).all()
+    assert (np.concatenate(outs_ip) == batched[: offsets[600]]).all()
+
+
+@pytest.mark.parametrize("mode", ["copy", "inplace"])
+def test_every_length_and_phase(P, cuda, mode):
+    """Lengths 0..300 at every in/out 16-byte phase (edge vectors, the
+    other-phase store path, tiles of one vector)."""
+    rng = np.random.default_rng(11)
+    base = torch.zeros(4096, dtype=torch.int16, device="cuda")
+    obase = torch.zeros(4096, dtype=torch.int16, device="cuda")
+    for n in list(range(0, 70)) + list(range(70, 301, 7)):
+        x = rng.choice(ALPHABET, n)
+        e = O.fix_scalar(x)
+        for pi in range(8):
+            po = (pi * 3 + n) % 8
+            src = base[pi:pi + n]
+            src.copy_(dev(x)) if n else None
+            if mode == "copy":
+                dst = obase[po + 16:po + 16 + n]
+                guard = obase.clone()
+                P.to_well_formed(src, out=dst)
+                got = host(dst)
+                # nothing outside [po+16, po+16+n) was touched
+                diff = (obase != guard).nonzero().flatten().tolist()
+                assert all(po + 16 <= i < po + 16 + n for i in diff)
+            else:
+                guard = base.clone()
+                P.to_well_formed_(src)
+                got = host(src)
+                diff = (base != guard).nonzero().flatten().tolist()
+                assert all(pi <= i < pi + n for i in diff)
+            assert (got == e).all(), (n, pi, po)
+
+
+def test_tile_boundaries_and_halos(P, cuda):
+    rng = np.random.default_rng(5)
+    for n in (8191, 8192, 8193, 8192 * 3 + 5, 1 << 20, 3_000_017):
+        x = rng.choice(ALPHABET, n)
+        e = O.stencil(x)
+        assert (gpu_copy(P, x) == e).all(), n
+        assert (gpu_inplace(P, x) == e).all(), n
+        # explicit halos: every combination at both ends
+        for left in (-1, 0x41, 0xD800, 0xDC00):
+            for right in (-1, 0x41, 0xD800, 0xDC00):
+                t = dev(x)
+                out = torch.empty_like(t)
+                P.to_well_formed_halo(t, out, left, right)
+                assert (host(out) == O.stencil(x, left, right)).all()
+                if n > 100_000:
+                    break
+
+
+def test_valid_pair_straddling_every_position(P, cuda):
+    """proj/tests/test_generic_kernel.cpp:113-127, across warp/CTA tiles."""
+    n = 2 * 8192 + 64
+    for pos in list(range(0, 300)) + list(range(1000, 1100)) + list(range(8150, 8250)) + [n - 2]:
+        x = np.full(n, 0x41, np.uint16)
+        x[pos], x[pos + 1] = 0xD83D, 0xDE0A
+        assert (gpu_copy(P, x) == x).all()
+        assert (gpu_inplace(P, x) == x).all()
+
+
+def test_well_formed_in_place_identity(P, cuda):
+    x = np.frombuffer(P.generate_utf16le(400_000, 0.05, 0.0, 77), np.uint16)
+    assert P.is_well_formed_utf16le(x.tobytes())
+    assert (gpu_inplace(P, x) == x).all()
+
+
+def test_count_and_offsets(P, cuda):
+    rng = np.random.default_rng(9)
+    for n in (1, 31, 1000, 8193, 100_003, 2_000_000):
+        x = rng.choice(ALPHABET, n)
+        e = O.unpaired_offsets(x)
+        t = dev(x)
+        assert P.count_unpaired(t) == len(e)
+        assert P.unpaired_offsets_device(t).cpu().tolist() == e
+        for lim in (0, 1, 7, 1000):
+            assert P.unpaired_offsets_device(t, lim).cpu().tolist() == e[:lim]
+    assert P.unpaired_surrogate_offsets(O.u16([0x41, 0xDC00, 0x42, 0xD800]).tobytes(), 1) == [1]
+
+
+def test_batched_edges(P, cuda):
+    rng = np.random.default_rng(21)
+    # string-edge semantics: H|L across an edge must both become FFFD
+    x = O.u16([0x41, 0xD800, 0xDC00, 0x42, 0xDC00, 0xD800])
+    for offs in ([0, 2, 4, 6], [0, 6], [1, 1, 3, 5], [0, 1, 2, 3, 4, 5, 6], [2, 2]):
+        o = np.array(offs, np.int64)
+        got = host(P.to_well_formed_batched(dev(x), torch.from_numpy(o).cuda()))
+        assert (got == O.fix_batched(x, o)).all(), offs
+    # random strings with empties and long strings, unaligned start
+    lens = rng.choice([0, 1, 2, 3, 7, 8, 9, 31, 100, 5000, 20000], 3000)
+    offsets = np.zeros(lens.size + 1, np.int64)
+    offsets[1:] = np.cumsum(lens) + 5
+    offsets[0] = 5
+    data = rng.choice(ALPHABET, int(offsets[-1]) + 9)
+    e = O.fix_batched(data, offsets)
+    got = host(P.to_well_formed_batched(dev(data), torch.from_numpy(offsets).cuda()))
+    assert (got == e).all()
+    assert (got[:5] == data[:5]).all() and (got[offsets[-1]:] == data[offsets[-1]:]).all()
+
+
+def test_errors(P, cuda):
+    t = torch.zeros(100, dtype=torch.int16, device="cuda")
+    with pytest.raises(ValueError):
+        P.to_well_formed(t[0:50], out=t[25:75])             # partial overlap
+    with pytest.raises(ValueError):
+        P.fix_utf16le(b"\x00\xd8\x41")                      # odd length
+    with pytest.raises(ValueError):
+        P.fix_utf16le(b"\x00\xd8", kernel="avx9000")        # unknown kernel
+    assert P.fix_utf16le(b"\x00\xd8", kernel="bitmask") == b"\xfd\xff"
+    with pytest.raises(ValueError):
+        P.to_well_formed(torch.zeros(4, dtype=torch.int16))  # host tensor to device API
+
+
+def test_host_pipeline_chunks(P, cuda):
+    """u16m_to_well_formed_host: > 2 chunks, pinned and pageable, copy and in place."""
+    n = (8 << 20) * 2 + 12345
+    x = O.gen_config(1, n, seed=77)
+    e = O.stencil_mt(x)
+    assert np.frombuffer(P.fix_utf16le(x.tobytes()), np.uint16).tobytes() == e.tobytes()
+    import ctypes
+    L = P._lib.raw()
+    pin = torch.from_numpy(x.view(np.int16)).pin_memory()
+    outp = torch.empty_like(pin).pin_memory()
+    assert L.u16m_to_well_formed_host(pin.data_ptr(), n, outp.data_ptr()) == 0
+    assert (outp.numpy().view(np.uint16) == e).all()
+    assert L.u16m_to_well_formed_host(pin.data_ptr(), n, pin.data_ptr()) == 0
+    assert (pin.numpy().view(np.uint16) == e).all()
+
+
+def test_sharded_virtual(P, cuda):
+    """u16m_to_well_formed_sharded with several shards on one GPU (device ids
+    repeat), including empty shards and adversarial shard-edge patterns."""
+    L = 1 << 16
+    for G in (1, 2, 4, 7):
+        total = G * L
+        x = O.gen_config(4, total, seed=4, shard_len=L)
+        e = O.stencil(x)
+        shards = [dev(x[g * L:(g + 1) * L]) for g in range(G)]
+        outs = [torch.empty_like(s) for s in shards]
+        P.to_well_formed_sharded(shards, outs)
+        assert (np.concatenate([host(o) for o in outs]) == e).all()
+        P.to_well_formed_sharded(shards)  # in place
+        assert (np.concatenate([host(s) for s in shards]) == e).all()
+    # ragged + empty shards
+    x = O.gen_config(4, 100_000, seed=4, shard_len=25_000)
+    cuts = [0, 0, 1, 24_999, 25_001, 25_001, 60_000, 100_000]
+    shards = [dev(x[a:b]) if b > a else torch.empty(0, dtype=torch.int16, device="cuda")
+              for a, b in zip(cuts[:-1], cuts[1:])]
+    P.to_well_formed_sharded(shards)
+    assert (np.concatenate([host(s) for s in shards]) == O.stencil(x)).all()
+
+
+def test_inplace_race_stress(P, cuda):
+    """In-place vs copy on the worst-case error density, repeated, different
+    sub-buffer offsets (changes the tile/warp-edge alignment every time)."""
+    n = 1 << 22
+    x = O.gen_config(1, n + 64, seed=1)
+    e_full = None
+    big = dev(x)
+    for off in (0, 1, 3, 7, 8, 13, 31, 33):
+        src = big[off:off + n]
+        ref = P.to_well_formed(src)
+        for rep in range(3):
+            t = src.clone()
+            P.to_well_formed_(t)
+            assert torch.equal(t, ref)
+        if off == 0:
+            e_full = O.stencil_mt(x[:n])
+            assert (host(ref) == e_full).all()
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 4])
+def test_device_generator_matches_oracle(P, cuda, cfg):
+    total = 3_000_000
+    shard = 1_000_000 if cfg == 4 else 0
+    g = host(P._lib.gen_config(cfg, total, shard_len=shard))
+    assert (g == O.gen_config(cfg, total, shard_len=shard)).all()
+    w = host(P._lib.gen_config(cfg, total, first=123_457, count=777_777, shard_len=shard))
+    assert (w == O.gen_config(cfg, total, first=123_457, count=777_777, shard_len=shard)).all()
+
+
+def test_device_c3_generator_matches_oracle(P, cuda):
+    d, o = P._lib.gen_c3(20_000)
+    hd, ho = O.gen_c3(20_000)
+    assert (o.cpu().numpy() == ho).all()
+    assert (host(d) == hd).all()
+
+
+# ---- BASELINE configs ---------------------------------------------------------
+def test_config0_full(P, cuda):
+    n = 1 << 24
+    x = O.gen_config(0, n, seed=0)
+    e = O.stencil_mt(x)
+    t = dev(x)
+    assert (host(P.to_well_formed(t)) == e).all()
+    assert (host(P.to_well_formed_(t)) == e).all()
+
+
+def _window_checks(P, x_dev, y_dev, n, rng, count=24, w=70_000):
+    """Exact oracle parity on random windows of a full-size result."""
+    starts = [0, n - w] + [int(s) for s in rng.integers(0, n - w, count)]
+    for a in starts:
+        b = a + w
+        xin = host(x_dev[a:b])
+        left = int(host(x_dev[a - 1:a])[0]) if a > 0 else -1
+        right = int(host(x_dev[b:b + 1])[0]) if b < n else -1
+        assert (host(y_dev[a:b]) == O.stencil(xin, left, right)).all(), a
+
+
+@pytest.mark.slow
+def test_config1_full_inplace(P, cuda):
+    n = 1 << 28
+    rng = np.random.default_rng(1)
+    x = P._lib.gen_config(1, n, seed=1)
+    y = x.clone()
+    P.to_well_formed_(y)
+    _window_checks(P, x, y, n, rng)
+    z = P.to_well_formed(x)
+    assert torch.equal(y, z)                              # in place == copy
+    assert P.count_unpaired(y) == 0                       # well-formed
+    assert P.count_unpaired(x) == int((x != y).sum())     # minimality count
+    assert torch.equal(P.to_well_formed(y), y)            # idempotence
+    frac = (x != y).float().mean().item()
+    assert 0.028 < frac < 0.034
+
+
+@pytest.mark.slow
+def test_config2_full_copy(P, cuda):
+    n = 1 << 29
+    rng = np.random.default_rng(2)
+    x = P._lib.gen_config(2, n, seed=2)
+    y = P.to_well_formed(x)
+    _window_checks(P, x, y, n, rng)
+    # every adversarial tile-boundary window (sampled) is exact
+    for t in rng.integers(1, n // 256, 200):
+        b = int(t) * 256
+        a = b - 8
+        xin = host(x[a:b + 8])
+        assert (host(y[a:b + 8]) == O.stencil(xin, int(host(x[a - 1:a])[0]), int(host(x[b + 8:b + 9])[0]))).all()
+    assert P.count_unpaired(y) == 0
+    assert torch.equal(P.to_well_formed(y), y)
+
+
+@pytest.mark.slow
+def test_config3_full_batched(P, cuda):
+    d, o = P._lib.gen_c3(1 << 20)
+    ho = o.cpu().numpy()
+    y = P.to_well_formed_batched(d, o)
+    hd, hy = host(d), host(y)
+    e = O.fix_batched(hd, ho)
+    assert (hy == e).all()
+    y2 = d.clone()
+    P.to_well_formed_batched(y2, o, out=y2)
+    assert torch.equal(y2, y)
+
+
+@pytest.mark.slow
+def test_config4_shards(P, cuda):
+    """Config 4 on one GPU: 4 virtual shards of 2^26 units with adversarial
+    shard edges (exact, whole buffer) and one full 2^32-unit shard (windows)."""
+    L, G = 1 << 26, 4
+    x = P._lib.gen_config(4, G * L, seed=4, shard_len=L)
+    e = O.stencil_mt(host(x))
+    shards = [x[g * L:(g + 1) * L].clone() for g in range(G)]
+    outs = [torch.empty_like(s) for s in shards]
+    P.to_well_formed_sharded(shards, outs)
+    assert (np.concatenate([host(o) for o in outs]) == e).all()
+    P.to_well_formed_sharded(shards)
+    assert (np.concatenate([host(s) for s in shards]) == e).all()
+    del x, shards, outs
+    torch.cuda.empty_cache()
+    n = 1 << 32
+    x = P._lib.gen_config(4, n, seed=4, shard_len=n)
+    y = P.to_well_formed(x)
+    _window_checks(P, x, y, n, np.random.default_rng(4), count=16)
+    assert P.count_unpaired(y) == 0
