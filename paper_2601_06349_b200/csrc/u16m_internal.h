@@ -14,6 +14,13 @@ namespace u16m {
 cudaError_t launch_repair(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
                           const uint16_t* left_ptr, const uint16_t* right_ptr, cudaStream_t stream);
 
+// TMA-pipelined forms (u16m_tma.cu); same 16-byte phase for in and out.
+constexpr size_t kTmaMinUnits = size_t(1) << 15;
+cudaError_t launch_repair_tma(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
+                              const uint16_t* left_ptr, const uint16_t* right_ptr, cudaStream_t stream);
+cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
+                               cudaStream_t stream);
+
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream);
 

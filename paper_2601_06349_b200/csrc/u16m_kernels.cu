@@ -29,6 +29,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "u16m_internal.h"
@@ -99,6 +101,63 @@ __device__ __forceinline__ void mask_outside(const Span& s, uint64_t vi, uint32_
   }
 }
 
+// Marks every string start of this CTA tile in `starts` (bit i = aligned unit
+// cta_v0*8 + i). Warp 0 searches; the CTA synchronises around it.
+__device__ __forceinline__ void mark_string_starts(const BatchArgs& b, uint64_t cta_v0, uint32_t* starts,
+                                                   int warp, int lane) {
+  __syncthreads();  // previous tile's readers are done with `starts`
+  if (warp == 0) {
+    for (int i = lane; i < kCtaUnits / 32 + 2; i += 32) starts[i] = 0;
+    __syncwarp();
+    const int64_t key_lo = static_cast<int64_t>(cta_v0 * 8) - static_cast<int64_t>(b.phase);
+    const int64_t key_hi = key_lo + kCtaUnits;
+    uint64_t sidx = warp_lower_bound(b.offsets, b.count, key_lo, lane);
+    for (;;) {
+      const uint64_t idx = sidx + lane;
+      const int64_t p = idx < b.count ? __ldg(b.offsets + idx) : INT64_MAX;
+      const bool inside = p <= key_hi;
+      if (inside) {
+        const uint64_t bit = static_cast<uint64_t>(p - key_lo);
+        atomicOr(&starts[bit >> 5], 1u << (bit & 31));
+      }
+      if (__ballot_sync(kFull, inside) != kFull) break;
+      sidx += 32;
+    }
+  }
+  __syncthreads();
+}
+
+// Bad-unit flags of the kVecs vectors of this lane, given their classified
+// flags and the warp tile's halo unit (lane 0: unit before the tile; lane 31:
+// unit after it).
+template <bool kBatched>
+__device__ __forceinline__ void tile_bad(const Flags (&f)[kVecs], uint32_t halo, int lane,
+                                         const uint32_t* starts, uint32_t a_base,
+                                         uint32_t (&B0)[kVecs], uint32_t (&B1)[kVecs]) {
+  const uint32_t halo_h = hflag_hi(halo);
+  const uint32_t halo_l = lflag_lo(halo);
+  uint32_t up[kVecs], dn[kVecs];
+#pragma unroll
+  for (int k = 0; k < kVecs; k++) {
+    up[k] = __shfl_sync(kFull, f[k].H1, (lane + 31) & 31);
+    dn[k] = __shfl_sync(kFull, f[k].L0, (lane + 1) & 31);
+  }
+#pragma unroll
+  for (int k = 0; k < kVecs; k++) {
+    const uint32_t hp = lane ? up[k] : (k ? up[k - 1] : halo_h);
+    const uint32_t ln = lane != 31 ? dn[k] : (k + 1 < kVecs ? dn[k + 1] : halo_l);
+    if constexpr (kBatched) {
+      const uint32_t a0 = a_base + static_cast<uint32_t>(k * 32 + lane) * 8;
+      const uint64_t pair = static_cast<uint64_t>(starts[a0 >> 5]) |
+                            (static_cast<uint64_t>(starts[(a0 >> 5) + 1]) << 32);
+      const uint32_t bits = static_cast<uint32_t>(pair >> (a0 & 31));
+      bad8(f[k], hp, ln, B0[k], B1[k], spread4(bits), spread4(bits >> 4), ((bits >> 8) & 1u) << 7);
+    } else {
+      bad8(f[k], hp, ln, B0[k], B1[k]);
+    }
+  }
+}
+
 template <int kMode, bool kSamePhase, bool kBatched>
 __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, ScanArgs sc) {
   constexpr bool kScanMode = kMode == kTileCount || kMode == kEmit;
@@ -120,11 +179,50 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
   const uint64_t vend = (s.hi + 7) / 8;
   const uint64_t ntiles = (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
   uint64_t counted = 0;
+  const uint32_t lane_off = static_cast<uint32_t>(warp * kWarpVecs + lane);  // vector offset in tile
 
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t cta_v0 = vbeg + tile * kCtaVecs;
     const uint64_t warp_v0 = cta_v0 + static_cast<uint64_t>(warp) * kWarpVecs;
+    // Interior tile: every vector full and both warp-tile halos in range.
+    const bool interior = cta_v0 * 8 > s.lo && (cta_v0 + kCtaVecs) * 8 < s.hi;
 
+    if (interior && (kMode == kCopy || kMode == kInPlace)) {
+      // ---- fast path: no range checks, one 64-bit base per lane ----
+      const uint4* src = s.in + cta_v0 + lane_off;
+      uint4 v[kVecs];
+#pragma unroll
+      for (int k = 0; k < kVecs; k++) v[k] = ld_stream(src + k * 32);
+      uint32_t halo = 0;
+      const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
+      if (lane == 0) halo = src16[-1];
+      if (lane == 31) halo = src16[(kVecs - 1) * 32 * 8 + 8];
+      if constexpr (kBatched) mark_string_starts(b, cta_v0, starts, warp, lane);
+      Flags f[kVecs];
+#pragma unroll
+      for (int k = 0; k < kVecs; k++) f[k] = classify8(v[k]);
+      uint32_t B0[kVecs], B1[kVecs];
+      tile_bad<kBatched>(f, halo, lane, starts, (lane_off - lane) * 8, B0, B1);
+      if constexpr (kSamePhase) {
+        uint4* dst = s.out + cta_v0 + lane_off;
+#pragma unroll
+        for (int k = 0; k < kVecs; k++) {
+          if (kMode == kInPlace && (B0[k] | B1[k]) == 0) continue;
+          st_stream(dst + k * 32, blend(v[k], B0[k], B1[k]));
+        }
+      } else {
+        uint16_t* dst = s.out_units + ((cta_v0 + lane_off) * 8 - s.lo);
+#pragma unroll
+        for (int k = 0; k < kVecs; k++) {
+          const uint4 r = blend(v[k], B0[k], B1[k]);
+#pragma unroll
+          for (int j = 0; j < 8; j++) dst[k * 256 + j] = static_cast<uint16_t>(get_unit(r, j));
+        }
+      }
+      continue;
+    }
+
+    // ---- general path: edge tiles, and the count / scan modes ----
     uint4 v[kVecs];
 #pragma unroll
     for (int k = 0; k < kVecs; k++) {
@@ -134,29 +232,7 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
     uint32_t halo = 0;
     if (lane == 0) halo = unit_at(s, static_cast<int64_t>(warp_v0 * 8) - 1);
     if (lane == 31) halo = unit_at(s, static_cast<int64_t>((warp_v0 + kWarpVecs) * 8));
-
-    if constexpr (kBatched) {
-      __syncthreads();  // previous tile's readers are done with `starts`
-      if (warp == 0) {
-        for (int i = lane; i < kCtaUnits / 32 + 2; i += 32) starts[i] = 0;
-        __syncwarp();
-        const int64_t key_lo = static_cast<int64_t>(cta_v0 * 8) - static_cast<int64_t>(b.phase);
-        const int64_t key_hi = key_lo + kCtaUnits;
-        uint64_t sidx = warp_lower_bound(b.offsets, b.count, key_lo, lane);
-        for (;;) {
-          const uint64_t idx = sidx + lane;
-          const int64_t p = idx < b.count ? __ldg(b.offsets + idx) : INT64_MAX;
-          const bool inside = p <= key_hi;
-          if (inside) {
-            const uint64_t bit = static_cast<uint64_t>(p - key_lo);
-            atomicOr(&starts[bit >> 5], 1u << (bit & 31));
-          }
-          if (__ballot_sync(kFull, inside) != kFull) break;
-          sidx += 32;
-        }
-      }
-      __syncthreads();
-    }
+    if constexpr (kBatched) mark_string_starts(b, cta_v0, starts, warp, lane);
 
     Flags f[kVecs];
     bool edge[kVecs];
@@ -167,32 +243,12 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
       if (edge[k]) patch_edges(s, vi, v[k]);
       f[k] = classify8(v[k]);
     }
-    const uint32_t halo_h = hflag_hi(halo);
-    const uint32_t halo_l = lflag_lo(halo);
-    uint32_t up[kVecs], dn[kVecs];
-#pragma unroll
-    for (int k = 0; k < kVecs; k++) {
-      up[k] = __shfl_sync(kFull, f[k].H1, (lane + 31) & 31);
-      dn[k] = __shfl_sync(kFull, f[k].L0, (lane + 1) & 31);
-    }
-
     uint32_t B0[kVecs], B1[kVecs];
+    tile_bad<kBatched>(f, halo, lane, starts, (lane_off - lane) * 8, B0, B1);
+    if constexpr (kMode >= kCount) {
 #pragma unroll
-    for (int k = 0; k < kVecs; k++) {
-      const uint64_t vi = warp_v0 + k * 32 + lane;
-      const uint32_t hp = lane ? up[k] : (k ? up[k - 1] : halo_h);
-      const uint32_t ln = lane != 31 ? dn[k] : (k + 1 < kVecs ? dn[k + 1] : halo_l);
-      if constexpr (kBatched) {
-        const uint32_t a0 = static_cast<uint32_t>((vi - cta_v0) * 8);
-        const uint64_t pair = static_cast<uint64_t>(starts[a0 >> 5]) |
-                              (static_cast<uint64_t>(starts[(a0 >> 5) + 1]) << 32);
-        const uint32_t bits = static_cast<uint32_t>(pair >> (a0 & 31));
-        bad8(f[k], hp, ln, B0[k], B1[k], spread4(bits), spread4(bits >> 4),
-             ((bits >> 8) & 1u) << 7);
-      } else {
-        bad8(f[k], hp, ln, B0[k], B1[k]);
-      }
-      if (kMode >= kCount && edge[k]) mask_outside(s, vi, B0[k], B1[k]);
+      for (int k = 0; k < kVecs; k++)
+        if (edge[k]) mask_outside(s, warp_v0 + k * 32 + lane, B0[k], B1[k]);
     }
 
     if constexpr (kMode == kCopy || kMode == kInPlace) {
@@ -340,11 +396,24 @@ uint64_t tiles_for(const Span& s) {
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Kernel family selection: "tma" (default; bulk-async pipelined, same-phase
+// buffers) or "ldg" (register-staged). U16M_KERNEL overrides, for A/B runs.
+static int kernel_choice() {
+  static const int choice = [] {
+    const char* e = std::getenv("U16M_KERNEL");
+    if (e && std::strcmp(e, "ldg") == 0) return 0;
+    return 1;
+  }();
+  return choice;
+}
+
 cudaError_t launch_repair(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
                           const uint16_t* left_ptr, const uint16_t* right_ptr, cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
   bool same = false;
   const Span s = make_span(in, n, out, left, right, left_ptr, right_ptr, &same);
+  if ((in == out || same) && kernel_choice() == 1 && n >= kTmaMinUnits)
+    return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
   const uint64_t grid = tiles_for(s);
   if (in == out) return launch<kInPlace, true, false>(s, kNoBatch, kNoScan, grid, stream);
   if (same) return launch<kCopy, true, false>(s, kNoBatch, kNoScan, grid, stream);
@@ -426,6 +495,8 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
 
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream) {
+  if (kernel_choice() == 1 && ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0)
+    return launch_batched_tma(in, offsets, num_strings, out, stream);
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
   const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
