@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
   __shared__ unsigned long long warp_sums[kScanMode ? kWarps : 1];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  // A concurrently launched body grid (u16m_body.cu) may start right away.
+  asm volatile("griddepcontrol.launch_dependents;");
 
   if constexpr (kBatched) {
     // Range of the batch, read on the device (no host sync in the API).
@@ -180,8 +182,10 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
   const uint64_t ntiles = (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
   uint64_t counted = 0;
   const uint32_t lane_off = static_cast<uint32_t>(warp * kWarpVecs + lane);  // vector offset in tile
+  const uint64_t nwork = s.edges_only ? (ntiles < 2 ? ntiles : 2) : ntiles;
 
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const uint64_t tile = s.edges_only && w == 1 ? ntiles - 1 : w;
     const uint64_t cta_v0 = vbeg + tile * kCtaVecs;
     const uint64_t warp_v0 = cta_v0 + static_cast<uint64_t>(warp) * kWarpVecs;
     // Interior tile: every vector full and both warp-tile halos in range.
@@ -383,6 +387,7 @@ Span make_span(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_
   s.right = right;
   s.left_ptr = left_ptr;
   s.right_ptr = right_ptr;
+  s.edges_only = 0;
   *same_phase = out != nullptr && ((ia & 15u) == (oa & 15u));
   return s;
 }
@@ -396,13 +401,16 @@ uint64_t tiles_for(const Span& s) {
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-// Kernel family selection: "tma" (default; bulk-async pipelined, same-phase
-// buffers) or "ldg" (register-staged). U16M_KERNEL overrides, for A/B runs.
+// Kernel family selection (U16M_KERNEL, for A/B runs): "body" (default:
+// lean interior kernel + edge-tile kernel), "tma" (bulk-async pipelined),
+// "general" (one general kernel for every tile).
+enum KernelChoice { kChoiceBody = 0, kChoiceTma = 1, kChoiceGeneral = 2 };
 static int kernel_choice() {
   static const int choice = [] {
     const char* e = std::getenv("U16M_KERNEL");
-    if (e && std::strcmp(e, "ldg") == 0) return 0;
-    return 1;
+    if (e && std::strcmp(e, "tma") == 0) return int(kChoiceTma);
+    if (e && std::strcmp(e, "general") == 0) return int(kChoiceGeneral);
+    return int(kChoiceBody);
   }();
   return choice;
 }
@@ -412,9 +420,21 @@ cudaError_t launch_repair(const uint16_t* in, size_t n, uint16_t* out, int32_t l
   if (n == 0) return cudaSuccess;
   bool same = false;
   const Span s = make_span(in, n, out, left, right, left_ptr, right_ptr, &same);
-  if ((in == out || same) && kernel_choice() == 1 && n >= kTmaMinUnits)
-    return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
   const uint64_t grid = tiles_for(s);
+  const int choice = kernel_choice();
+  if ((in == out || same) && choice == kChoiceTma && n >= kTmaMinUnits)
+    return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
+  if ((in == out || same) && choice == kChoiceBody && grid > 2) {
+    // Edge tiles (first, last) on the general kernel, every other tile on the
+    // lean body kernel; PDL lets the body grid start while the edge grid runs.
+    Span e = s;
+    e.edges_only = 1;
+    cudaError_t err = in == out ? launch<kInPlace, true, false>(e, kNoBatch, kNoScan, 2, stream)
+                                : launch<kCopy, true, false>(e, kNoBatch, kNoScan, 2, stream);
+    if (err != cudaSuccess) return err;
+    err = launch_body(s.in, s.out, s.lo / 8 + kCtaVecs, grid - 2, in == out, stream);
+    return err != cudaSuccess ? err : cudaGetLastError();
+  }
   if (in == out) return launch<kInPlace, true, false>(s, kNoBatch, kNoScan, grid, stream);
   if (same) return launch<kCopy, true, false>(s, kNoBatch, kNoScan, grid, stream);
   return launch<kCopy, false, false>(s, kNoBatch, kNoScan, grid, stream);
@@ -495,7 +515,7 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
 
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream) {
-  if (kernel_choice() == 1 && ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0)
+  if (kernel_choice() == kChoiceTma && ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0)
     return launch_batched_tma(in, offsets, num_strings, out, stream);
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
@@ -507,6 +527,7 @@ cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t nu
   s.lo = s.hi = 0;
   s.left = s.right = -1;
   s.left_ptr = s.right_ptr = nullptr;
+  s.edges_only = 0;
   const BatchArgs b{offsets, static_cast<uint64_t>(num_strings) + 1, ph};
   // Persistent grid: the range is only known on the device.
   const uint64_t grid = static_cast<uint64_t>(sm_count_for_current_device()) * 8;

@@ -41,6 +41,7 @@ struct Span {
   int32_t left, right;     // halo unit values, -1 = outside the logical buffer
   const uint16_t* left_ptr;   // device-side halo (overrides left/right if set)
   const uint16_t* right_ptr;
+  int edges_only;          // 1: process only the first and the last tile
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
