@@ -17,13 +17,24 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "u16m_internal.h"
 #include "u16m_repair.cuh"
 
 namespace u16m {
 
-template <bool kInPlace>
+// In-place write-back granularity in lanes of 16 B (U16M_GRAN: 1, 2, 4, 8).
+int inplace_granularity() {
+  static const int g = [] {
+    const char* e = std::getenv("U16M_GRAN");
+    const int v = e ? std::atoi(e) : kDefaultInplaceGran;
+    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : kDefaultInplaceGran;
+  }();
+  return g;
+}
+
+template <bool kInPlace, int kGran>
 __global__ void __launch_bounds__(kThreads) body_kernel(const uint4* __restrict__ in, uint4* out,
                                                         uint64_t first_vec) {
   const int lane = threadIdx.x & 31;
@@ -58,7 +69,7 @@ __global__ void __launch_bounds__(kThreads) body_kernel(const uint4* __restrict_
     uint32_t B0, B1;
     bad8(f[k], hp, ln, B0, B1);
     if (kInPlace) {
-      if (B0 | B1) st_stream(dst + k * 32, blend(v[k], B0, B1));
+      if (group_dirty<kGran>((B0 | B1) != 0, lane)) st_stream(dst + k * 32, blend(v[k], B0, B1));
     } else {
       st_stream(dst + k * 32, blend(v[k], B0, B1));
     }
@@ -77,8 +88,17 @@ cudaError_t launch_body(const uint4* in, uint4* out, uint64_t first_vec, uint64_
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = in_place ? cudaLaunchKernelEx(&cfg, body_kernel<true>, in, out, first_vec)
-                           : cudaLaunchKernelEx(&cfg, body_kernel<false>, in, out, first_vec);
+  cudaError_t e;
+  if (!in_place) {
+    e = cudaLaunchKernelEx(&cfg, body_kernel<false, 1>, in, out, first_vec);
+  } else {
+    switch (inplace_granularity()) {
+      case 1: e = cudaLaunchKernelEx(&cfg, body_kernel<true, 1>, in, out, first_vec); break;
+      case 2: e = cudaLaunchKernelEx(&cfg, body_kernel<true, 2>, in, out, first_vec); break;
+      case 8: e = cudaLaunchKernelEx(&cfg, body_kernel<true, 8>, in, out, first_vec); break;
+      default: e = cudaLaunchKernelEx(&cfg, body_kernel<true, 4>, in, out, first_vec); break;
+    }
+  }
   note_launch();
   return e;
 }

@@ -24,6 +24,9 @@ cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream);
 
+constexpr int kDefaultInplaceGran = 4;
+int inplace_granularity();
+
 // Lean interior-tile kernel (u16m_body.cu): tiles [first_vec, first_vec +
 // ntiles*kCtaVecs) of 16-byte-aligned in/out, all interior. PDL launch.
 cudaError_t launch_body(const uint4* in, uint4* out, uint64_t first_vec, uint64_t ntiles, bool in_place,

@@ -163,6 +163,22 @@ __device__ __forceinline__ uint32_t lflag_lo(uint32_t u) {  // L(u) in byte lane
   return ((u & 0xFC00u) == 0xDC00u) ? 0x80u : 0u;
 }
 
+// In-place store policy: a lane writes its vector back when any lane of its
+// aligned group of kGran lanes (kGran*16 contiguous bytes) holds a rewrite.
+// kGran = 1 writes only dirty 16-byte vectors; larger groups trade extra
+// bytes for whole-burst DRAM writes instead of scattered partial sectors.
+// All 32 lanes must call it (warp ballot).
+template <int kGran>
+__device__ __forceinline__ bool group_dirty(bool dirty, int lane) {
+  if constexpr (kGran == 1) {
+    return dirty;
+  } else {
+    const uint32_t m = __ballot_sync(kFull, dirty);
+    const uint32_t g = (kGran >= 32 ? 0xFFFFFFFFu : ((1u << kGran) - 1u)) << (lane & ~(kGran - 1));
+    return (m & g) != 0;
+  }
+}
+
 // 4 bits -> bit 7 of byte lanes 0..3.
 __device__ __forceinline__ uint32_t spread4(uint32_t bits) {
   return (((bits & 0xFu) * 0x00204081u) & 0x01010101u) << 7;

@@ -136,7 +136,7 @@ __device__ __forceinline__ uint64_t lower_bound32(const int64_t* off, uint64_t c
   return m ? lo + (__ffs(m) - 1) : hi;
 }
 
-template <int kInPlace, bool kBatched>
+template <int kInPlace, bool kBatched, int kGran>
 __global__ void __launch_bounds__(kThreadsTma, 2) repair_tma_kernel(Span s, BatchArgsT b) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kThreadsTma, 2) repair_tma_kernel(Span s, Batc
       } else {
         bad8(f[k], hp, ln, B0, B1);
       }
-      if (kInPlace && (B0 | B1) == 0) continue;
+      if (kInPlace && !group_dirty<kGran>((B0 | B1) != 0, lane)) continue;
       const uint4 r = blend(v[k], B0, B1);
       if (!edge[k]) {
         if (interior || tv0 + lane_off + k * 32 < vend) st_stream(dst + k * 32, r);
@@ -297,9 +297,9 @@ __global__ void __launch_bounds__(kThreadsTma, 2) repair_tma_kernel(Span s, Batc
 
 std::mutex g_mu;
 int g_sms[64] = {0};
-bool g_attr_set[4][64] = {};
+bool g_attr_set[4][64][9] = {};
 
-template <int kInPlace, bool kBatched>
+template <int kInPlace, bool kBatched, int kGran>
 cudaError_t launch_tma(const Span& s, const BatchArgsT& b, uint64_t ntiles_hint, cudaStream_t stream) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -307,19 +307,19 @@ cudaError_t launch_tma(const Span& s, const BatchArgsT& b, uint64_t ntiles_hint,
   {
     std::lock_guard<std::mutex> lock(g_mu);
     const int idx = kInPlace * 2 + (kBatched ? 1 : 0);
-    if (dev < 64 && !g_attr_set[idx][dev]) {
-      e = cudaFuncSetAttribute(repair_tma_kernel<kInPlace, kBatched>,
+    if (dev < 64 && !g_attr_set[idx][dev][kGran]) {
+      e = cudaFuncSetAttribute(repair_tma_kernel<kInPlace, kBatched, kGran>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
       if (e != cudaSuccess) return e;
       int n = 0;
       cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
       g_sms[dev] = n > 0 ? n : 148;
-      g_attr_set[idx][dev] = true;
+      g_attr_set[idx][dev][kGran] = true;
     }
   }
   uint64_t grid = static_cast<uint64_t>(dev < 64 ? g_sms[dev] : 148) * 2;
   if (ntiles_hint > 0 && ntiles_hint < grid) grid = ntiles_hint;
-  repair_tma_kernel<kInPlace, kBatched><<<static_cast<unsigned>(grid), kThreadsTma, kSmemBytes, stream>>>(s, b);
+  repair_tma_kernel<kInPlace, kBatched, kGran><<<static_cast<unsigned>(grid), kThreadsTma, kSmemBytes, stream>>>(s, b);
   note_launch();
   return cudaGetLastError();
 }
@@ -344,8 +344,13 @@ cudaError_t launch_repair_tma(const uint16_t* in, size_t n, uint16_t* out, int32
   s.edges_only = 0;
   const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kCtaVecs - 1) / kCtaVecs;
   const tma::BatchArgsT b{nullptr, 0, 0};
-  if (in == out) return tma::launch_tma<1, false>(s, b, ntiles, stream);
-  return tma::launch_tma<0, false>(s, b, ntiles, stream);
+  if (in != out) return tma::launch_tma<0, false, 1>(s, b, ntiles, stream);
+  switch (inplace_granularity()) {
+    case 1: return tma::launch_tma<1, false, 1>(s, b, ntiles, stream);
+    case 2: return tma::launch_tma<1, false, 2>(s, b, ntiles, stream);
+    case 8: return tma::launch_tma<1, false, 8>(s, b, ntiles, stream);
+    default: return tma::launch_tma<1, false, 4>(s, b, ntiles, stream);
+  }
 }
 
 cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
@@ -362,8 +367,8 @@ cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_
   s.left_ptr = s.right_ptr = nullptr;
   s.edges_only = 0;
   const tma::BatchArgsT b{offsets, static_cast<uint64_t>(num_strings) + 1, ph};
-  if (in == out) return tma::launch_tma<1, true>(s, b, 0, stream);
-  return tma::launch_tma<0, true>(s, b, 0, stream);
+  if (in == out) return tma::launch_tma<1, true, 1>(s, b, 0, stream);
+  return tma::launch_tma<0, true, 1>(s, b, 0, stream);
 }
 
 }  // namespace u16m
