@@ -34,28 +34,31 @@ int inplace_granularity() {
   return g;
 }
 
-template <bool kInPlace, int kGran>
-__global__ void __launch_bounds__(kThreads) body_kernel(const uint4* __restrict__ in, uint4* out,
-                                                        uint64_t first_vec) {
+// kV vectors per thread; a CTA always covers one 1024-vector tile, so the
+// block has 1024/kV threads (U16M_BODY_VECS selects 2, 4 or 8 for A/B runs).
+template <bool kInPlace, int kGran, int kV>
+__global__ void __launch_bounds__(kCtaVecs / kV) body_kernel(const uint4* __restrict__ in, uint4* out,
+                                                             uint64_t first_vec) {
+  constexpr int kWV = 32 * kV;  // vectors per warp tile
   const int lane = threadIdx.x & 31;
-  const uint32_t lane_off = threadIdx.x / 32 * kWarpVecs + lane;
+  const uint32_t lane_off = threadIdx.x / 32 * kWV + lane;
   const uint64_t v0 = first_vec + static_cast<uint64_t>(blockIdx.x) * kCtaVecs + lane_off;
   const uint4* src = in + v0;
 
-  uint4 v[kVecs];
+  uint4 v[kV];
 #pragma unroll
-  for (int k = 0; k < kVecs; k++) v[k] = ld_stream(src + k * 32);
+  for (int k = 0; k < kV; k++) v[k] = ld_stream(src + k * 32);
   const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
   uint32_t halo = 0;
   if (lane == 0) halo = src16[-1];
-  if (lane == 31) halo = src16[(kVecs - 1) * 32 * 8 + 8];
+  if (lane == 31) halo = src16[(kV - 1) * 32 * 8 + 8];
 
-  Flags f[kVecs];
+  Flags f[kV];
 #pragma unroll
-  for (int k = 0; k < kVecs; k++) f[k] = classify8(v[k]);
-  uint32_t up[kVecs], dn[kVecs];
+  for (int k = 0; k < kV; k++) f[k] = classify8(v[k]);
+  uint32_t up[kV], dn[kV];
 #pragma unroll
-  for (int k = 0; k < kVecs; k++) {
+  for (int k = 0; k < kV; k++) {
     up[k] = __shfl_sync(kFull, f[k].H1, (lane + 31) & 31);
     dn[k] = __shfl_sync(kFull, f[k].L0, (lane + 1) & 31);
   }
@@ -63,9 +66,9 @@ __global__ void __launch_bounds__(kThreads) body_kernel(const uint4* __restrict_
   const uint32_t halo_l = lflag_lo(halo);
   uint4* dst = out + v0;
 #pragma unroll
-  for (int k = 0; k < kVecs; k++) {
+  for (int k = 0; k < kV; k++) {
     const uint32_t hp = lane ? up[k] : (k ? up[k - 1] : halo_h);
-    const uint32_t ln = lane != 31 ? dn[k] : (k + 1 < kVecs ? dn[k + 1] : halo_l);
+    const uint32_t ln = lane != 31 ? dn[k] : (k + 1 < kV ? dn[k + 1] : halo_l);
     uint32_t B0, B1;
     bad8(f[k], hp, ln, B0, B1);
     if (kInPlace) {
@@ -76,12 +79,33 @@ __global__ void __launch_bounds__(kThreads) body_kernel(const uint4* __restrict_
   }
 }
 
+static int body_vecs() {
+  static const int v = [] {
+    const char* e = std::getenv("U16M_BODY_VECS");
+    const int x = e ? std::atoi(e) : 4;
+    return (x == 2 || x == 4 || x == 8) ? x : 4;
+  }();
+  return v;
+}
+
+template <int kV>
+static cudaError_t launch_body_v(cudaLaunchConfig_t& cfg, const uint4* in, uint4* out, uint64_t first_vec,
+                                 bool in_place) {
+  cfg.blockDim = dim3(kCtaVecs / kV);
+  if (!in_place) return cudaLaunchKernelEx(&cfg, body_kernel<false, 1, kV>, in, out, first_vec);
+  switch (inplace_granularity()) {
+    case 1: return cudaLaunchKernelEx(&cfg, body_kernel<true, 1, kV>, in, out, first_vec);
+    case 4: return cudaLaunchKernelEx(&cfg, body_kernel<true, 4, kV>, in, out, first_vec);
+    case 8: return cudaLaunchKernelEx(&cfg, body_kernel<true, 8, kV>, in, out, first_vec);
+    default: return cudaLaunchKernelEx(&cfg, body_kernel<true, 2, kV>, in, out, first_vec);
+  }
+}
+
 cudaError_t launch_body(const uint4* in, uint4* out, uint64_t first_vec, uint64_t ntiles, bool in_place,
                         cudaStream_t stream) {
   if (ntiles == 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(ntiles));
-  cfg.blockDim = dim3(kThreads);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -89,15 +113,10 @@ cudaError_t launch_body(const uint4* in, uint4* out, uint64_t first_vec, uint64_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;
-  if (!in_place) {
-    e = cudaLaunchKernelEx(&cfg, body_kernel<false, 1>, in, out, first_vec);
-  } else {
-    switch (inplace_granularity()) {
-      case 1: e = cudaLaunchKernelEx(&cfg, body_kernel<true, 1>, in, out, first_vec); break;
-      case 2: e = cudaLaunchKernelEx(&cfg, body_kernel<true, 2>, in, out, first_vec); break;
-      case 8: e = cudaLaunchKernelEx(&cfg, body_kernel<true, 8>, in, out, first_vec); break;
-      default: e = cudaLaunchKernelEx(&cfg, body_kernel<true, 4>, in, out, first_vec); break;
-    }
+  switch (body_vecs()) {
+    case 2: e = launch_body_v<2>(cfg, in, out, first_vec, in_place); break;
+    case 8: e = launch_body_v<8>(cfg, in, out, first_vec, in_place); break;
+    default: e = launch_body_v<4>(cfg, in, out, first_vec, in_place); break;
   }
   note_launch();
   return e;

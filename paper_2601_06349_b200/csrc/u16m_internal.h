@@ -24,7 +24,7 @@ cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream);
 
-constexpr int kDefaultInplaceGran = 4;
+constexpr int kDefaultInplaceGran = 2;
 int inplace_granularity();
 
 // Lean interior-tile kernel (u16m_body.cu): tiles [first_vec, first_vec +
