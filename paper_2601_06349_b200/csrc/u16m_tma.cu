@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(kThreadsTma, 2) repair_tma_kernel(Span s, Batc
   const uint64_t vbeg = s.lo / 8;
   const uint64_t vend = (s.hi + 7) / 8;
   const uint64_t ntiles = (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
+  const uint64_t t_begin = ntiles * blockIdx.x / gridDim.x;
+  const uint64_t t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; i++) {
@@ -162,8 +164,20 @@ __global__ void __launch_bounds__(kThreadsTma, 2) repair_tma_kernel(Span s, Batc
 
   if (warp == kConsumerWarps) {
     // ------------------------------ producer ------------------------------
+    // This CTA owns the contiguous tiles [t_begin, t_end); the batched form
+    // searches `offsets` once and then walks it forward tile by tile, with
+    // the next tile's 32-entry window prefetched while the ring is full.
     uint32_t it = 0;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+    uint64_t sidx = 0;
+    int64_t win = INT64_MAX;
+    if constexpr (kBatched) {
+      if (t_begin < t_end) {
+        const int64_t key0 = static_cast<int64_t>((vbeg + t_begin * kCtaVecs) * 8) - static_cast<int64_t>(b.phase);
+        sidx = lower_bound32(b.offsets, b.count, key0, lane);
+        win = sidx + lane < b.count ? __ldg(b.offsets + sidx + lane) : INT64_MAX;
+      }
+    }
+    for (uint64_t tile = t_begin; tile < t_end; tile++, it++) {
       const int st = it % kStages;
       const uint32_t phase = (it / kStages) & 1u;
       unsigned char* stage = smem + st * kStageStride;
@@ -183,18 +197,21 @@ __global__ void __launch_bounds__(kThreadsTma, 2) repair_tma_kernel(Span s, Batc
         __syncwarp();
         const int64_t key_lo = static_cast<int64_t>(tv0 * 8) - static_cast<int64_t>(b.phase);
         const int64_t key_hi = key_lo + kCtaUnits;
-        uint64_t sidx = lower_bound32(b.offsets, b.count, key_lo, lane);
+        uint64_t scan = sidx, next = sidx;
+        int64_t p = win;
         for (;;) {
-          const uint64_t idx = sidx + lane;
-          const int64_t p = idx < b.count ? __ldg(b.offsets + idx) : INT64_MAX;
           const bool inside = p <= key_hi;
           if (inside) {
             const uint64_t bit = static_cast<uint64_t>(p - key_lo);
             atomicOr(&bits[bit >> 5], 1u << (bit & 31));
           }
+          next += __popc(__ballot_sync(kFull, p < key_hi));
           if (__ballot_sync(kFull, inside) != kFull) break;
-          sidx += 32;
+          scan += 32;
+          p = scan + lane < b.count ? __ldg(b.offsets + scan + lane) : INT64_MAX;
         }
+        sidx = next;  // first string starting at or after the next tile's first unit
+        win = sidx + lane < b.count ? __ldg(b.offsets + sidx + lane) : INT64_MAX;  // prefetch
         __syncwarp();
         if (lane == 0) mbar_arrive(fbar);  // release: bitmap visible to the consumers
       }
@@ -205,7 +222,7 @@ __global__ void __launch_bounds__(kThreadsTma, 2) repair_tma_kernel(Span s, Batc
   // ------------------------------ consumers -------------------------------
   const uint32_t lane_off = static_cast<uint32_t>(warp * kWarpVecs + lane);
   uint32_t it = 0;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+  for (uint64_t tile = t_begin; tile < t_end; tile++, it++) {
     const int st = it % kStages;
     const uint32_t phase = (it / kStages) & 1u;
     unsigned char* stage = smem + st * kStageStride;
