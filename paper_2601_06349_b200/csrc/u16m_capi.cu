@@ -79,13 +79,19 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
   } while (0)
 
 // ---- host staging pipeline -------------------------------------------------
-constexpr int kPipeStreams = 4;
-constexpr size_t kChunkUnits = size_t(8) << 20;  // 16 MiB per chunk
+// Three streams (H2D copy engine, compute, D2H copy engine) over a ring of
+// device chunk buffers, ordered by events: chunk c's H2D waits only for the
+// D2H that last used its buffer, so the host->device and device->host copy
+// engines both stay busy (PCIe full duplex) while the kernel runs between
+// them.
+constexpr int kRing = 16;
+constexpr size_t kChunkUnits = size_t(4) << 20;  // 8 MiB per chunk
 
 struct HostPipe {
   int device = -1;
-  cudaStream_t streams[kPipeStreams] = {};
-  uint16_t* dbuf[kPipeStreams] = {};
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  uint16_t* dbuf[kRing] = {};
+  cudaEvent_t loaded[kRing] = {}, repaired[kRing] = {}, drained[kRing] = {};
 };
 
 std::mutex g_pipe_mu;
@@ -96,13 +102,18 @@ HostPipe* pipe_for(int device, u16m_status* st) {
     if (p->device == device) return p;
   auto* p = new HostPipe;
   p->device = device;
-  for (int i = 0; i < kPipeStreams; i++) {
-    cudaError_t e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMalloc(&p->dbuf[i], kChunkUnits * sizeof(uint16_t));
-    if (e != cudaSuccess) {
-      *st = cuda_fail(e, "host pipeline setup");
-      return nullptr;
-    }
+  cudaError_t e = cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking);
+  for (int i = 0; i < kRing && e == cudaSuccess; i++) {
+    e = cudaMalloc(&p->dbuf[i], kChunkUnits * sizeof(uint16_t));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->loaded[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->repaired[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->drained[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    *st = cuda_fail(e, "host pipeline setup");
+    return nullptr;
   }
   g_pipes.push_back(p);
   return p;
@@ -247,24 +258,32 @@ u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out
   size_t c = 0;
   for (size_t c0 = 0; c0 < n; c0 += kChunkUnits, c++) {
     const size_t len = std::min(kChunkUnits, n - c0);
-    const int k = static_cast<int>(c % kPipeStreams);
-    cudaStream_t s = p->streams[k];
+    const int k = static_cast<int>(c % kRing);
     // Halo units are read from the host copy at enqueue time. For in-place
     // jobs an earlier chunk's D2H may already have rewritten in[c0-1]; that
     // is benign (a unit is only rewritten when no neighbour pairs with it).
     const int32_t left = c0 > 0 ? static_cast<int32_t>(in[c0 - 1]) : -1;
     const int32_t right = c0 + len < n ? static_cast<int32_t>(in[c0 + len]) : -1;
-    e = cudaMemcpyAsync(p->dbuf[k], in + c0, len * 2, cudaMemcpyHostToDevice, s);
+    if (c >= static_cast<size_t>(kRing)) {
+      e = cudaStreamWaitEvent(p->h2d, p->drained[k], 0);
+      if (e != cudaSuccess) return cuda_fail(e, "pipeline wait");
+    }
+    e = cudaMemcpyAsync(p->dbuf[k], in + c0, len * 2, cudaMemcpyHostToDevice, p->h2d);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-    e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, s);
+    cudaEventRecord(p->loaded[k], p->h2d);
+    cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
+    e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, p->comp);
     if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
-    e = cudaMemcpyAsync(out + c0, p->dbuf[k], len * 2, cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(p->repaired[k], p->comp);
+    cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
+    e = cudaMemcpyAsync(out + c0, p->dbuf[k], len * 2, cudaMemcpyDeviceToHost, p->d2h);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    cudaEventRecord(p->drained[k], p->d2h);
   }
-  for (int k = 0; k < kPipeStreams; k++) {
-    e = cudaStreamSynchronize(p->streams[k]);
-    if (e != cudaSuccess) return cuda_fail(e, "host pipeline sync");
-  }
+  e = cudaStreamSynchronize(p->d2h);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->h2d);
+  if (e != cudaSuccess) return cuda_fail(e, "host pipeline sync");
   return U16M_OK;
 }
 
