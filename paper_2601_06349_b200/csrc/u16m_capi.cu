@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -85,7 +86,19 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // engines both stay busy (PCIe full duplex) while the kernel runs between
 // them.
 constexpr int kRing = 16;
-constexpr size_t kChunkUnits = size_t(4) << 20;  // 8 MiB per chunk
+constexpr size_t kChunkUnits = size_t(8) << 20;  // ring buffer size: 16 MiB
+
+// Pipeline chunk in units (U16M_PIPE_CHUNK_KIB overrides; at most kChunkUnits).
+size_t pipe_chunk_units() {
+  static const size_t c = [] {
+    const char* e = std::getenv("U16M_PIPE_CHUNK_KIB");
+    size_t kib = e ? static_cast<size_t>(std::atoll(e)) : 8192;
+    size_t u = kib * 512;
+    if (u < 4096) u = 4096;
+    return u > kChunkUnits ? kChunkUnits : u;
+  }();
+  return c;
+}
 
 struct HostPipe {
   int device = -1;
@@ -256,8 +269,9 @@ u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out
   HostPipe* p = pipe_for(dev, &st);
   if (p == nullptr) return st;
   size_t c = 0;
-  for (size_t c0 = 0; c0 < n; c0 += kChunkUnits, c++) {
-    const size_t len = std::min(kChunkUnits, n - c0);
+  const size_t chunk = pipe_chunk_units();
+  for (size_t c0 = 0; c0 < n; c0 += chunk, c++) {
+    const size_t len = std::min(chunk, n - c0);
     const int k = static_cast<int>(c % kRing);
     // Halo units are read from the host copy at enqueue time. For in-place
     // jobs an earlier chunk's D2H may already have rewritten in[c0-1]; that
