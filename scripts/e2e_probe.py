@@ -1,0 +1,29 @@
+"""Probe the host-staged e2e path (u16m_to_well_formed_host) on this box."""
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2601_06349_b200 import _lib  # noqa: E402
+
+L = _lib.raw()
+n = 1 << 28
+x = _lib.gen_config(1, n, seed=1)
+h = torch.empty(n, dtype=torch.int16, pin_memory=True)
+h.copy_(x)
+src = h.clone().pin_memory()
+out = torch.empty_like(h).pin_memory()
+for mode in ("inplace", "copy"):
+    times = []
+    for i in range(8):
+        if mode == "inplace":
+            h.copy_(src)
+        t = time.perf_counter()
+        st = L.u16m_to_well_formed_host(h.data_ptr(), n, (h if mode == "inplace" else out).data_ptr())
+        times.append(time.perf_counter() - t)
+        assert st == 0
+    best = min(times[2:])
+    print(os.environ.get("U16M_PIPE_CHUNK_KIB", "default"), mode,
+          f"{2 * n / best / 1e9:.1f} GB/s best, {2 * n * 6 / sum(times[2:]) / 1e9:.1f} mean")
