@@ -85,14 +85,14 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // D2H that last used its buffer, so the host->device and device->host copy
 // engines both stay busy (PCIe full duplex) while the kernel runs between
 // them.
-constexpr int kRing = 16;
-constexpr size_t kChunkUnits = size_t(8) << 20;  // ring buffer size: 16 MiB
+constexpr int kRing = 8;
+constexpr size_t kChunkUnits = size_t(32) << 20;  // ring buffer size: 64 MiB
 
 // Pipeline chunk in units (U16M_PIPE_CHUNK_KIB overrides; at most kChunkUnits).
 size_t pipe_chunk_units() {
   static const size_t c = [] {
     const char* e = std::getenv("U16M_PIPE_CHUNK_KIB");
-    size_t kib = e ? static_cast<size_t>(std::atoll(e)) : 8192;
+    size_t kib = e ? static_cast<size_t>(std::atoll(e)) : 32768;
     size_t u = kib * 512;
     if (u < 4096) u = 4096;
     return u > kChunkUnits ? kChunkUnits : u;
