@@ -75,6 +75,19 @@ u16m_status u16m_to_well_formed_halo_ptr(const uint16_t* in, size_t n, uint16_t*
                                          const uint16_t* left_ptr, const uint16_t* right_ptr,
                                          void* stream);
 
+/* Split form of u16m_to_well_formed_halo_ptr for overlapping a halo exchange
+ * with the bulk of the work. The job's 8192-unit tiles are cut into
+ * U16M_PART_INTERIOR (every tile except the first and the last; reads no
+ * halo) and U16M_PART_EDGES (the first and last tiles; the only part that
+ * reads left_ptr / right_ptr). The two parts write disjoint units and may
+ * run concurrently on different streams; INTERIOR + EDGES == ALL. */
+#define U16M_PART_ALL 0
+#define U16M_PART_EDGES 1
+#define U16M_PART_INTERIOR 2
+u16m_status u16m_to_well_formed_part(const uint16_t* in, size_t n, uint16_t* out,
+                                     const uint16_t* left_ptr, const uint16_t* right_ptr, int part,
+                                     void* stream);
+
 /* NEW (north star item 5): one logical buffer split into contiguous shards
  * resident on (possibly) different GPUs of this process. Shard g lives on
  * device device_ids[g]; shard_out[g] == shard_in[g] for in-place. Halo units

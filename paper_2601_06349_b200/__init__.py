@@ -35,6 +35,7 @@ from ._lib import (  # noqa: F401
     to_well_formed_,
     to_well_formed_batched,
     to_well_formed_halo,
+    to_well_formed_part,
     to_well_formed_sharded,
     unpaired_offsets_device,
     unpaired_surrogate_offsets,
@@ -52,6 +53,7 @@ __all__ = [
     "to_well_formed",
     "to_well_formed_",
     "to_well_formed_halo",
+    "to_well_formed_part",
     "to_well_formed_batched",
     "to_well_formed_sharded",
     "count_unpaired",

@@ -34,6 +34,7 @@ _L.u16m_to_well_formed_in_place.argtypes = [_u16p, _sz, _vp]
 _L.u16m_to_well_formed_batched.argtypes = [_u16p, _vp, _sz, _u16p, _vp]
 _L.u16m_to_well_formed_halo.argtypes = [_u16p, _sz, _u16p, ctypes.c_int32, ctypes.c_int32, _vp]
 _L.u16m_to_well_formed_halo_ptr.argtypes = [_u16p, _sz, _u16p, _vp, _vp, _vp]
+_L.u16m_to_well_formed_part.argtypes = [_u16p, _sz, _u16p, _vp, _vp, ctypes.c_int, _vp]
 _L.u16m_to_well_formed_sharded.argtypes = [ctypes.c_int, _vp, _vp, _vp, _vp]
 _L.u16m_to_well_formed_host.argtypes = [_u16p, _sz, _u16p]
 _L.u16m_count_unpaired.argtypes = [_u16p, _sz, _vp, _vp]
@@ -51,7 +52,7 @@ _L.u16m_generate_reference_mix.argtypes = [_sz, ctypes.c_double, ctypes.c_double
 _L.u16m_l2_flush.argtypes = [_vp, _sz, _vp]
 for _f in ("u16m_to_well_formed", "u16m_to_well_formed_in_place", "u16m_to_well_formed_batched",
            "u16m_to_well_formed_halo", "u16m_to_well_formed_halo_ptr", "u16m_to_well_formed_sharded",
-           "u16m_to_well_formed_host", "u16m_count_unpaired", "u16m_unpaired_offsets",
+           "u16m_to_well_formed_host", "u16m_to_well_formed_part", "u16m_count_unpaired", "u16m_unpaired_offsets",
            "u16m_gen_config", "u16m_gen_c3_offsets", "u16m_gen_c3_content",
            "u16m_generate_reference_mix", "u16m_l2_flush"):
     getattr(_L, _f).restype = _st
@@ -144,6 +145,21 @@ def to_well_formed_halo(x: torch.Tensor, out: Optional[torch.Tensor], left: int,
     with torch.cuda.device(x.device):
         _check(_L.u16m_to_well_formed_halo(x.data_ptr(), x.numel(), out.data_ptr(), int(left), int(right),
                                            _stream(x, stream)))
+    return out
+
+
+PART_ALL, PART_EDGES, PART_INTERIOR = 0, 1, 2
+
+
+def to_well_formed_part(x: torch.Tensor, out: Optional[torch.Tensor], part: int, left_ptr: int = 0,
+                        right_ptr: int = 0, stream=None) -> torch.Tensor:
+    """One part (PART_EDGES / PART_INTERIOR / PART_ALL) of a shard repair; halo
+    units are read on the device from left_ptr / right_ptr (0 = buffer end)."""
+    _units(x, "x")
+    out = x if out is None else _units(out, "out")
+    with torch.cuda.device(x.device):
+        _check(_L.u16m_to_well_formed_part(x.data_ptr(), x.numel(), out.data_ptr(), left_ptr or None,
+                                           right_ptr or None, int(part), _stream(x, stream)))
     return out
 
 

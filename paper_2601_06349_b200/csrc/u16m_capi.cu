@@ -191,6 +191,21 @@ u16m_status u16m_to_well_formed_halo_ptr(const uint16_t* in, size_t n, uint16_t*
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "repair kernel launch");
 }
 
+u16m_status u16m_to_well_formed_part(const uint16_t* in, size_t n, uint16_t* out,
+                                     const uint16_t* left_ptr, const uint16_t* right_ptr, int part,
+                                     void* stream) {
+  if (part != U16M_PART_ALL && part != U16M_PART_EDGES && part != U16M_PART_INTERIOR)
+    return fail(U16M_ERR_INVALID_ARGUMENT, "part must be U16M_PART_ALL, _EDGES or _INTERIOR");
+  U16M_TRY(check_pair(in, n, out));
+  if (n == 0) return U16M_OK;
+  U16M_TRY(check_device_present());
+  U16M_TRY(check_device_ptr(in, "in"));
+  if (out != in) U16M_TRY(check_device_ptr(out, "out"));
+  const cudaError_t e =
+      u16m::launch_repair_part(in, n, out, -1, -1, left_ptr, right_ptr, part, as_stream(stream));
+  return e == cudaSuccess ? U16M_OK : cuda_fail(e, "repair kernel launch");
+}
+
 u16m_status u16m_to_well_formed_halo(const uint16_t* in, size_t n, uint16_t* out, int32_t left,
                                      int32_t right, void* stream) {
   if (left > 0xFFFF || right > 0xFFFF || left < -1 || right < -1)

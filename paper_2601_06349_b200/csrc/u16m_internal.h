@@ -27,10 +27,12 @@ cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t nu
 constexpr int kDefaultInplaceGran = 2;
 int inplace_granularity();
 
-// Lean interior-tile kernel (u16m_body.cu): tiles [first_vec, first_vec +
-// ntiles*kCtaVecs) of 16-byte-aligned in/out, all interior. PDL launch.
-cudaError_t launch_body(const uint4* in, uint4* out, uint64_t first_vec, uint64_t ntiles, bool in_place,
-                        cudaStream_t stream);
+// Part of a job: part = 0 all tiles, 1 only the two edge tiles (the only
+// ones that read the halos), 2 only the interior tiles. Edges + interior ==
+// all; the two parts write disjoint units and may run concurrently.
+cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
+                               const uint16_t* left_ptr, const uint16_t* right_ptr, int part,
+                               cudaStream_t stream);
 
 cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
                                   cudaStream_t stream);

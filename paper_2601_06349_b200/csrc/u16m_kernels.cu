@@ -158,15 +158,13 @@ __device__ __forceinline__ void tile_bad(const Flags (&f)[kVecs], uint32_t halo,
   }
 }
 
-template <int kMode, bool kSamePhase, bool kBatched>
+template <int kMode, bool kSamePhase, bool kBatched, int kGran = 1>
 __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, ScanArgs sc) {
   constexpr bool kScanMode = kMode == kTileCount || kMode == kEmit;
   __shared__ uint32_t starts[kBatched ? (kCtaUnits / 32 + 2) : 1];
   __shared__ unsigned long long warp_sums[kScanMode ? kWarps : 1];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  // A concurrently launched body grid (u16m_body.cu) may start right away.
-  asm volatile("griddepcontrol.launch_dependents;");
 
   if constexpr (kBatched) {
     // Range of the batch, read on the device (no host sync in the API).
@@ -182,10 +180,17 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
   const uint64_t ntiles = (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
   uint64_t counted = 0;
   const uint32_t lane_off = static_cast<uint32_t>(warp * kWarpVecs + lane);  // vector offset in tile
-  const uint64_t nwork = s.edges_only ? (ntiles < 2 ? ntiles : 2) : ntiles;
+  // Tile selection: all tiles, only the two edge tiles, or only the interior
+  // tiles (the last two let a caller overlap a halo exchange with the body).
+  uint64_t nwork = ntiles, tbase = 0;
+  if (s.tile_sel == kTilesEdges) nwork = ntiles < 2 ? ntiles : 2;
+  if (s.tile_sel == kTilesInterior) {
+    nwork = ntiles > 2 ? ntiles - 2 : 0;
+    tbase = 1;
+  }
 
   for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-    const uint64_t tile = s.edges_only && w == 1 ? ntiles - 1 : w;
+    const uint64_t tile = s.tile_sel == kTilesEdges && w == 1 ? ntiles - 1 : tbase + w;
     const uint64_t cta_v0 = vbeg + tile * kCtaVecs;
     const uint64_t warp_v0 = cta_v0 + static_cast<uint64_t>(warp) * kWarpVecs;
     // Interior tile: every vector full and both warp-tile halos in range.
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
         uint4* dst = s.out + cta_v0 + lane_off;
 #pragma unroll
         for (int k = 0; k < kVecs; k++) {
-          if (kMode == kInPlace && (B0[k] | B1[k]) == 0) continue;
+          if (kMode == kInPlace && !group_dirty<kGran>((B0[k] | B1[k]) != 0, lane)) continue;
           st_stream(dst + k * 32, blend(v[k], B0[k], B1[k]));
         }
       } else {
@@ -358,12 +363,12 @@ int sm_count_for_current_device() {
   return cached[dev];
 }
 
-template <int kMode, bool kSamePhase, bool kBatched>
+template <int kMode, bool kSamePhase, bool kBatched, int kGran = 1>
 cudaError_t launch(const Span& s, const BatchArgs& b, const ScanArgs& sc, uint64_t grid,
                    cudaStream_t stream) {
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7FFFFFFFull) grid = 0x7FFFFFFFull;
-  repair_kernel<kMode, kSamePhase, kBatched>
+  repair_kernel<kMode, kSamePhase, kBatched, kGran>
       <<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(s, b, sc);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -387,7 +392,7 @@ Span make_span(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_
   s.right = right;
   s.left_ptr = left_ptr;
   s.right_ptr = right_ptr;
-  s.edges_only = 0;
+  s.tile_sel = kTilesAll;
   *same_phase = out != nullptr && ((ia & 15u) == (oa & 15u));
   return s;
 }
@@ -401,13 +406,15 @@ uint64_t tiles_for(const Span& s) {
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-// Kernel family selection. Default ("auto"): copy / in-place run the lean
-// register-staged body kernel + edge-tile kernel (measured best for plain
-// streams: 6.8 TB/s copy), the batched form runs the TMA-pipelined kernel
+// Kernel family selection. Default ("auto"): copy / in-place run the
+// register-staged kernel (measured best for plain streams: 6.8 TB/s copy,
+// interior tiles on a lean path), the batched form runs the TMA-pipelined kernel
 // (its producer warp walks the offsets off the consumers' critical path).
 // U16M_KERNEL overrides for A/B runs: "tma" (TMA for everything), "general"
 // (the general register-staged kernel for everything).
 enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2 };
+// (kChoiceGeneral and kChoiceAuto share the register-staged kernel for plain
+// streams; they differ for the batched form.)
 static int kernel_choice() {
   static const int choice = [] {
     const char* e = std::getenv("U16M_KERNEL");
@@ -418,29 +425,53 @@ static int kernel_choice() {
   return choice;
 }
 
-cudaError_t launch_repair(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
-                          const uint16_t* left_ptr, const uint16_t* right_ptr, cudaStream_t stream) {
+// In-place write-back granularity in lanes of 16 B (U16M_GRAN: 1, 2, 4, 8).
+int inplace_granularity() {
+  static const int g = [] {
+    const char* e = std::getenv("U16M_GRAN");
+    const int v = e ? std::atoi(e) : kDefaultInplaceGran;
+    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : kDefaultInplaceGran;
+  }();
+  return g;
+}
+
+template <int kGran>
+static cudaError_t launch_inplace(const Span& s, uint64_t grid, cudaStream_t stream) {
+  return launch<kInPlace, true, false, kGran>(s, kNoBatch, kNoScan, grid, stream);
+}
+
+cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
+                               const uint16_t* left_ptr, const uint16_t* right_ptr, int part,
+                               cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
   bool same = false;
-  const Span s = make_span(in, n, out, left, right, left_ptr, right_ptr, &same);
-  const uint64_t grid = tiles_for(s);
+  Span s = make_span(in, n, out, left, right, left_ptr, right_ptr, &same);
+  const uint64_t ntiles = tiles_for(s);
   const int choice = kernel_choice();
-  if ((in == out || same) && choice == kChoiceTma && n >= kTmaMinUnits)
+  if ((in == out || same) && choice == kChoiceTma && n >= kTmaMinUnits) {
+    // The TMA kernel has no tile selection: it does the whole job as "edges".
+    if (part == kTilesInterior) return cudaSuccess;
     return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
-  if ((in == out || same) && choice == kChoiceAuto && grid > 2) {
-    // Edge tiles (first, last) on the general kernel, every other tile on the
-    // lean body kernel; PDL lets the body grid start while the edge grid runs.
-    Span e = s;
-    e.edges_only = 1;
-    cudaError_t err = in == out ? launch<kInPlace, true, false>(e, kNoBatch, kNoScan, 2, stream)
-                                : launch<kCopy, true, false>(e, kNoBatch, kNoScan, 2, stream);
-    if (err != cudaSuccess) return err;
-    err = launch_body(s.in, s.out, s.lo / 8 + kCtaVecs, grid - 2, in == out, stream);
-    return err != cudaSuccess ? err : cudaGetLastError();
   }
-  if (in == out) return launch<kInPlace, true, false>(s, kNoBatch, kNoScan, grid, stream);
+  s.tile_sel = part;
+  const uint64_t grid = part == kTilesAll ? ntiles
+                        : part == kTilesEdges ? (ntiles < 2 ? ntiles : 2)
+                                              : (ntiles > 2 ? ntiles - 2 : 0);
+  if (in == out) {
+    switch (inplace_granularity()) {
+      case 1: return launch_inplace<1>(s, grid, stream);
+      case 4: return launch_inplace<4>(s, grid, stream);
+      case 8: return launch_inplace<8>(s, grid, stream);
+      default: return launch_inplace<2>(s, grid, stream);
+    }
+  }
   if (same) return launch<kCopy, true, false>(s, kNoBatch, kNoScan, grid, stream);
   return launch<kCopy, false, false>(s, kNoBatch, kNoScan, grid, stream);
+}
+
+cudaError_t launch_repair(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
+                          const uint16_t* left_ptr, const uint16_t* right_ptr, cudaStream_t stream) {
+  return launch_repair_part(in, n, out, left, right, left_ptr, right_ptr, kTilesAll, stream);
 }
 
 cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
@@ -530,7 +561,7 @@ cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t nu
   s.lo = s.hi = 0;
   s.left = s.right = -1;
   s.left_ptr = s.right_ptr = nullptr;
-  s.edges_only = 0;
+  s.tile_sel = kTilesAll;
   const BatchArgs b{offsets, static_cast<uint64_t>(num_strings) + 1, ph};
   // Persistent grid: the range is only known on the device.
   const uint64_t grid = static_cast<uint64_t>(sm_count_for_current_device()) * 8;

@@ -41,8 +41,10 @@ struct Span {
   int32_t left, right;     // halo unit values, -1 = outside the logical buffer
   const uint16_t* left_ptr;   // device-side halo (overrides left/right if set)
   const uint16_t* right_ptr;
-  int edges_only;          // 1: process only the first and the last tile
+  int tile_sel;            // kTilesAll / kTilesEdges / kTilesInterior
 };
+
+enum TileSel : int { kTilesAll = 0, kTilesEdges = 1, kTilesInterior = 2 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;

@@ -358,7 +358,7 @@ cudaError_t launch_repair_tma(const uint16_t* in, size_t n, uint16_t* out, int32
   s.right = right;
   s.left_ptr = left_ptr;
   s.right_ptr = right_ptr;
-  s.edges_only = 0;
+  s.tile_sel = kTilesAll;
   const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kCtaVecs - 1) / kCtaVecs;
   const tma::BatchArgsT b{nullptr, 0, 0};
   if (in != out) return tma::launch_tma<0, false, 1>(s, b, ntiles, stream);
@@ -382,7 +382,7 @@ cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_
   s.lo = s.hi = 0;
   s.left = s.right = -1;
   s.left_ptr = s.right_ptr = nullptr;
-  s.edges_only = 0;
+  s.tile_sel = kTilesAll;
   const tma::BatchArgsT b{offsets, static_cast<uint64_t>(num_strings) + 1, ph};
   if (in == out) return tma::launch_tma<1, true, 1>(s, b, 0, stream);
   return tma::launch_tma<0, true, 1>(s, b, 0, stream);

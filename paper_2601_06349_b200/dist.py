@@ -44,9 +44,9 @@ def gather_edges(shard: torch.Tensor, group=None, device: Optional[torch.device]
     e = edge_tensor(shard)
     if device is not None:
         e = e.to(device)
-    out = torch.empty((world, 2), dtype=torch.int32, device=e.device)
+    out = torch.empty(world * 2, dtype=torch.int32, device=e.device)
     dist.all_gather_into_tensor(out, e, group=group)
-    return out
+    return out.view(world, 2)
 
 
 def halos_from_edges(edges: torch.Tensor, rank: int) -> tuple[int, int]:
@@ -76,26 +76,50 @@ def halo_pointers(edges: torch.Tensor, rank: int) -> tuple[int, int]:
     return left, right
 
 
+_side_streams: dict = {}
+
+
+def _side_stream(device: torch.device) -> torch.cuda.Stream:
+    if device not in _side_streams:
+        _side_streams[device] = torch.cuda.Stream(device=device)
+    return _side_streams[device]
+
+
 def repair_shard(shard: torch.Tensor, out: Optional[torch.Tensor] = None, group=None, compute=None,
-                 all_nonempty: bool = True):
+                 all_nonempty: bool = True, overlap: bool = True):
     """Repair this rank's shard of the logical buffer.
 
-    Default: the sm_100a kernel through the C ABI, reading the neighbours'
-    units from the gathered device tensor (no host sync; requires every
-    rank's shard to be non-empty — pass all_nonempty=False otherwise).
-    `compute(shard, out, left, right)` replaces the kernel (CPU tests)."""
+    Default (sm_100a kernel through the C ABI, every rank's shard non-empty):
+    the interior tiles — everything except the shard's first and last
+    8192-unit tiles, and the only part that needs no halo — start at once on
+    the current stream, while a side stream all-gathers the edge units and
+    then repairs the two edge tiles reading the neighbours' units straight
+    from the gathered device tensor; the current stream joins the side
+    stream. No host synchronisation inside the step. overlap=False runs
+    gather -> whole-shard kernel serially.
+    `compute(shard, out, left, right)` replaces the kernel (CPU tests; host
+    halo values)."""
     rank = dist.get_rank(group)
     out = shard if out is None else out
-    edges = gather_edges(shard, group)
     if compute is None and all_nonempty and shard.numel() > 0:
         from . import _lib
 
-        lp, rp = halo_pointers(edges, rank)
-        st = _lib.raw().u16m_to_well_formed_halo_ptr(
-            shard.data_ptr(), shard.numel(), out.data_ptr(), lp or None, rp or None,
-            torch.cuda.current_stream(shard.device).cuda_stream)
-        _lib._check(st)
+        main = torch.cuda.current_stream(shard.device)
+        if not overlap:
+            edges = gather_edges(shard, group)
+            lp, rp = halo_pointers(edges, rank)
+            return _lib.to_well_formed_part(shard, out, _lib.PART_ALL, lp, rp)
+        side = _side_stream(shard.device)
+        side.wait_stream(main)
+        _lib.to_well_formed_part(shard, out, _lib.PART_INTERIOR, stream=main)
+        with torch.cuda.stream(side):
+            edges = gather_edges(shard, group)
+            lp, rp = halo_pointers(edges, rank)
+            _lib.to_well_formed_part(shard, out, _lib.PART_EDGES, lp, rp, stream=side)
+        edges.record_stream(side)
+        main.wait_stream(side)
         return out
+    edges = gather_edges(shard, group)
     left, right = halos_from_edges(edges, rank)
     if compute is None:
         from . import _lib

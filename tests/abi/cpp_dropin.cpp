@@ -1,0 +1,46 @@
+// Source written against the REFERENCE's driver.hpp API (proj/include/
+// utf16mend/driver.hpp:64-69) — compiled unchanged against include/utf16mend/
+// driver.hpp and linked to libu16m.so. Exit codes: 0 = repaired correctly,
+// 3 = std::runtime_error (no CUDA device: the path has no CPU fallback),
+// 1 = wrong result, 2 = wrong exception.
+#include <cstdio>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "utf16mend/driver.hpp"
+
+int main() {
+  using namespace utf16mend;
+  std::vector<char16_t> in;
+  for (const char c : std::string("Hello, world!Hello, world!Hello")) in.push_back(static_cast<char16_t>(c));
+  in[10] = 0xD800;
+  in[21] = 0xDC00;
+  in[29] = 0xD83D;
+  in[30] = 0xDE0A;
+  std::vector<char16_t> expected = in;
+  expected[10] = expected[21] = 0xFFFD;
+  std::vector<char16_t> out(in.size());
+  // length mismatch is std::invalid_argument before any device work
+  try {
+    std::vector<char16_t> short_out(3);
+    to_well_formed(in, short_out);
+    return 2;
+  } catch (const std::invalid_argument&) {
+  }
+  try {
+    to_well_formed(in, out, kernel_id::bitmask());
+    std::vector<char16_t> buf = in;
+    to_well_formed_in_place(buf, parse_kernel_id("generic8"));
+    if (out != expected || buf != expected) return 1;
+    std::printf("repaired %s\n", to_string(select_kernel()).c_str());
+    return 0;
+  } catch (const std::runtime_error& e) {
+    std::printf("runtime_error: %s\n", e.what());
+    return 3;
+  } catch (...) {
+    return 2;
+  }
+}

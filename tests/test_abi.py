@@ -1,0 +1,103 @@
+"""CPU: the C-ABI library loads, exports every symbol include/*.h declares,
+validates arguments and fails loudly (no CPU fallback) without a GPU; the
+source-compatible C++ header compiles and links; Python-level error
+behaviour matches the reference bindings."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2601_06349_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+INC = os.path.join(ROOT, "include")
+LIBDIR = os.path.join(ROOT, "paper_2601_06349_b200")
+
+
+def declared(header):
+    text = open(os.path.join(INC, header)).read()
+    return sorted(set(re.findall(r"\b(u16m_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.mark.parametrize("header", ["u16m.h", "u16m_datagen.h"])
+def test_exports_every_declared_symbol(header):
+    lib = ctypes.CDLL(P.lib_path())
+    names = declared(header)
+    assert len(names) >= 4
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", P.lib_path()], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}\b", out), n
+
+
+def test_cpp_api_symbols_exported():
+    out = subprocess.run(["nm", "-DC", "--defined-only", P.lib_path()], capture_output=True, text=True).stdout
+    for sym in ("utf16mend::to_well_formed(", "utf16mend::to_well_formed_in_place(",
+                "utf16mend::to_well_formed_batched(", "utf16mend::parse_kernel_id(",
+                "utf16mend::select_kernel(", "utf16mend::available_kernels(",
+                "utf16mend::is_well_formed(", "utf16mend::unpaired_surrogate_offsets("):
+        assert sym in out, sym
+
+
+def _has_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # noqa: BLE001
+        return False
+
+
+def test_c_consumer(tmp_path):
+    exe = tmp_path / "c_abi"
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", INC, os.path.join(ROOT, "tests", "abi", "c_abi.c"),
+                    "-L", LIBDIR, "-lu16m", f"-Wl,-rpath,{LIBDIR}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == (0 if _has_gpu() else 3), r.stdout + r.stderr
+
+
+def test_cpp_dropin_compiles_links_runs(tmp_path):
+    exe = tmp_path / "cpp_dropin"
+    subprocess.run(["g++", "-std=c++20", "-Wall", "-I", INC, os.path.join(ROOT, "tests", "abi", "cpp_dropin.cpp"),
+                    "-L", LIBDIR, "-lu16m", f"-Wl,-rpath,{LIBDIR}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    if _has_gpu():
+        assert r.returncode == 0, r.stdout + r.stderr
+    else:
+        assert r.returncode == 3 and "no CUDA device" in r.stdout, r.stdout + r.stderr
+
+
+def test_python_errors_match_reference_bindings():
+    with pytest.raises(ValueError, match="even length"):
+        P.fix_utf16le(b"\x41")                          # module.cpp:25-26
+    with pytest.raises(ValueError, match="unknown kernel"):
+        P.fix_utf16le(b"\x41\x00", kernel="nope")       # module.cpp:45
+    with pytest.raises(ValueError):
+        P.generate_utf16le(4, pair_pct=1.5)             # module.cpp:83-84
+    assert P.fix_utf16le(b"") == b""
+    assert P.available_kernels() == ["cuda-sm100a"]
+
+
+def test_no_cpu_fallback_without_gpu():
+    if _has_gpu():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        P.fix_utf16le(b"\x00\xd8")
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        P.fix_str("a\ud800")
+
+
+def test_generate_utf16le_matches_reference_generator():
+    for seed, n, p, m in ((0, 1000, 0.1, 0.3), (3, 50_000, 0.001, 0.0), (9, 17, 0.5, 0.5)):
+        a = np.frombuffer(P.generate_utf16le(n, p, m, seed), np.uint16)
+        assert (a == O.ref_generate(n, p, m, seed)).all()
+
+
+def test_header_is_plain_c():
+    text = open(os.path.join(INC, "u16m.h")).read()
+    assert "torch" not in text and "cuda_runtime" not in text and "extern \"C\"" in text

@@ -384,3 +384,25 @@ def test_config4_shards(P, cuda):
     y = P.to_well_formed(x)
     _window_checks(P, x, y, n, np.random.default_rng(4), count=16)
     assert P.count_unpaired(y) == 0
+
+
+def test_parts_on_two_streams(P, cuda):
+    """INTERIOR and EDGES parts run concurrently on two streams and together
+    equal the whole-job repair (the overlap used by dist.repair_shard)."""
+    rng = np.random.default_rng(31)
+    for n in (5, 8192, 8193, 3 * 8192, 100_003, 1 << 20):
+        x = O.gen_config(1, n, seed=n)
+        left, right = 0xD812, 0xDC34
+        hal = dev(np.array([left, right], np.uint16))
+        lp, rp = hal.data_ptr(), hal.data_ptr() + 2
+        e = O.stencil(x, left, right)
+        for in_place in (False, True):
+            t = dev(x)
+            out = t if in_place else torch.empty_like(t)
+            s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+            s1.wait_stream(torch.cuda.current_stream())
+            s2.wait_stream(torch.cuda.current_stream())
+            P.to_well_formed_part(t, out, P._lib.PART_INTERIOR, stream=s1)
+            P.to_well_formed_part(t, out, P._lib.PART_EDGES, lp, rp, stream=s2)
+            torch.cuda.synchronize()
+            assert (host(out) == e).all(), (n, in_place)
