@@ -34,6 +34,11 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
                                const uint16_t* left_ptr, const uint16_t* right_ptr, int part,
                                cudaStream_t stream);
 
+// Rolling-pipeline streaming kernel (u16m_stream.cu) for same-phase copy and
+// in-place jobs; `s` from make_span, part as in launch_repair_part.
+struct Span;
+cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream);
+
 cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
                                   cudaStream_t stream);
 
