@@ -38,6 +38,8 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
 // in-place jobs; `s` from make_span, part as in launch_repair_part.
 struct Span;
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream);
+// Warp-pipelined cp.async kernel (u16m_pipe.cu): whole same-phase jobs.
+cudaError_t launch_pipe(const Span& s, cudaStream_t stream);
 
 cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
                                   cudaStream_t stream);

@@ -412,7 +412,7 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 // (its producer warp walks the offsets off the consumers' critical path).
 // U16M_KERNEL overrides for A/B runs: "tma" (TMA for everything), "general"
 // (the general register-staged kernel for everything).
-enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2 };
+enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoiceStream = 3 };
 // (kChoiceGeneral and kChoiceAuto share the register-staged kernel for plain
 // streams; they differ for the batched form.)
 static int kernel_choice() {
@@ -420,6 +420,7 @@ static int kernel_choice() {
     const char* e = std::getenv("U16M_KERNEL");
     if (e && std::strcmp(e, "tma") == 0) return int(kChoiceTma);
     if (e && std::strcmp(e, "general") == 0) return int(kChoiceGeneral);
+    if (e && std::strcmp(e, "stream") == 0) return int(kChoiceStream);
     return int(kChoiceAuto);
   }();
   return choice;
@@ -453,7 +454,9 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
     if (part == kTilesInterior) return cudaSuccess;
     return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
   }
-  if ((in == out || same) && choice == kChoiceAuto) return launch_stream(s, part, stream);
+  if ((in == out || same) && choice == kChoiceAuto && part == kTilesAll) return launch_pipe(s, stream);
+  if ((in == out || same) && (choice == kChoiceAuto || choice == kChoiceStream))
+    return launch_stream(s, part, stream);
   s.tile_sel = part;
   const uint64_t grid = part == kTilesAll ? ntiles
                         : part == kTilesEdges ? (ntiles < 2 ? ntiles : 2)

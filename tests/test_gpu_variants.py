@@ -17,8 +17,9 @@ VARIANTS = [
     {"U16M_GRAN": "1"},
     {"U16M_GRAN": "4"},
     {"U16M_GRAN": "8"},
-    {"U16M_BODY_VECS": "2"},
-    {"U16M_BODY_VECS": "8", "U16M_GRAN": "4"},
+    {"U16M_KERNEL": "stream"},
+    {"U16M_KERNEL": "stream", "U16M_GRAN": "1"},
+    {"U16M_GRAN": "4", "U16M_PIPE_CHUNK_KIB": "64"},
 ]
 
 
