@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "u16m_internal.h"
@@ -52,7 +53,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
-template <bool kInPlace, int kGran>
+template <bool kInPlace, int kGran, bool kInterleave>
 __global__ void __launch_bounds__(kPThreads, kCtasPerSm) pipe_kernel(Span s) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
@@ -62,22 +63,34 @@ __global__ void __launch_bounds__(kPThreads, kCtasPerSm) pipe_kernel(Span s) {
   const uint64_t nstages = (vend - vbeg + kStageVecs - 1) / kStageVecs;
   const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kPWarps + warp;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kPWarps;
-  const uint64_t c0 = nstages * gw / nw, c1 = nstages * (gw + 1) / nw;  // this warp's chain
+  // Work items i = c0 .. c1-1 map to stages stage_of(i): a contiguous chain
+  // per warp, or (kInterleave) stages gw, gw + nw, gw + 2nw, ... so that the
+  // whole grid streams one neighbourhood of DRAM at a time.
+  uint64_t c0, c1;
+  if (kInterleave) {
+    c0 = 0;
+    c1 = gw < nstages ? (nstages - gw + nw - 1) / nw : 0;
+  } else {
+    c0 = nstages * gw / nw;
+    c1 = nstages * (gw + 1) / nw;
+  }
   if (c0 >= c1) return;
+  auto stage_of = [&](uint64_t i) { return kInterleave ? gw + i * nw : i; };
   const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(smem)) + warp * kSmemPerWarp + lane * 16;
 
-  auto issue = [&](uint64_t st) {  // copy this lane's kPV vectors of stage st
-    if (st < c1) {
-      const uint32_t slot = ring + static_cast<uint32_t>(st % kD) * (kStageVecs * 16);
-      const uint64_t v0 = vbeg + st * kStageVecs + lane;
+  auto issue = [&](uint64_t i) {  // copy this lane's kPV vectors of item i
+    if (i < c1) {
+      const uint32_t slot = ring + static_cast<uint32_t>(i % kD) * (kStageVecs * 16);
+      const uint64_t v0 = vbeg + stage_of(i) * kStageVecs + lane;
 #pragma unroll
       for (int k = 0; k < kPV; k++)
         if (v0 + k * 32 < vend) cp_async16(slot + k * 512, s.in + v0 + k * 32);
     }
     cp_commit();  // one group per stage, empty groups keep the count uniform
   };
-  auto fetch = [&](uint64_t st, uint4 (&v)[kPV]) {
-    const uint32_t slot = ring + static_cast<uint32_t>(st % kD) * (kStageVecs * 16);
+  auto fetch = [&](uint64_t i, uint4 (&v)[kPV]) {
+    const uint64_t st = stage_of(i);
+    const uint32_t slot = ring + static_cast<uint32_t>(i % kD) * (kStageVecs * 16);
 #pragma unroll
     for (int k = 0; k < kPV; k++) v[k] = lds128(slot + k * 512);
     const uint64_t v0 = vbeg + st * kStageVecs + lane;
@@ -95,30 +108,33 @@ __global__ void __launch_bounds__(kPThreads, kCtasPerSm) pipe_kernel(Span s) {
 
   // Look-behind of the chain's first unit (lane 0) — a global 2-byte read.
   uint32_t hp_carry = 0;
-  if (lane == 0) hp_carry = hflag_hi(unit_at(s, static_cast<int64_t>((vbeg + c0 * kStageVecs) * 8) - 1));
+  if (lane == 0) hp_carry = hflag_hi(unit_at(s, static_cast<int64_t>((vbeg + stage_of(c0) * kStageVecs) * 8) - 1));
 
   uint4 v[kPV];
   cp_wait<kD - 1>();
   fetch(c0, v);
   Flags cur = classify8(v[0]);
 
-  for (uint64_t st = c0; st < c1; st++) {
+  for (uint64_t i = c0; i < c1; i++) {
+    const uint64_t st = stage_of(i);
     // Flags of the next stage's first vector (look-ahead for lane 31's last).
     uint4 vn[kPV];
     Flags first_next;
-    const bool has_next = st + 1 < c1;
+    const bool has_next = i + 1 < c1;
     if (has_next) {
       cp_wait<kD - 2>();
-      fetch(st + 1, vn);
+      fetch(i + 1, vn);
       first_next = classify8(vn[0]);
     }
     uint32_t ln_tail;
     {
       const uint32_t dn_first = __shfl_sync(kFull, has_next ? first_next.L0 : 0u, (lane + 1) & 31);
       ln_tail = dn_first;
-      if (!has_next && lane == 31)
+      if ((kInterleave || !has_next) && lane == 31)
         ln_tail = lflag_lo(unit_at(s, static_cast<int64_t>((vbeg + (st + 1) * kStageVecs) * 8)));
     }
+    if (kInterleave && lane == 0 && i > c0)
+      hp_carry = hflag_hi(unit_at(s, static_cast<int64_t>((vbeg + st * kStageVecs) * 8) - 1));
     const uint64_t v0 = vbeg + st * kStageVecs + lane;
     const bool stage_interior =
         (vbeg + st * kStageVecs) * 8 >= s.lo && (vbeg + (st + 1) * kStageVecs) * 8 <= s.hi;
@@ -156,7 +172,7 @@ __global__ void __launch_bounds__(kPThreads, kCtasPerSm) pipe_kernel(Span s) {
       }
       if (k + 1 < kPV) cur = nxt;
     }
-    issue(st + kD);  // stage st's slot is free: every v[k] has been consumed
+    issue(i + kD);  // item i's slot is free: every v[k] has been consumed
     if (has_next) {
 #pragma unroll
       for (int k = 0; k < kPV; k++) v[k] = vn[k];
@@ -168,9 +184,17 @@ __global__ void __launch_bounds__(kPThreads, kCtasPerSm) pipe_kernel(Span s) {
 
 std::mutex g_mu;
 int g_sms[64] = {0};
-bool g_ready[64][2][9] = {};
+bool g_ready[64][2][9][2] = {};
 
-template <bool kInPlace, int kGran>
+static bool interleave() {
+  static const bool v = [] {
+    const char* e = std::getenv("U16M_PIPE_CHAIN");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
+
+template <bool kInPlace, int kGran, bool kIL>
 cudaError_t launch_t(const Span& s, cudaStream_t stream) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -178,14 +202,14 @@ cudaError_t launch_t(const Span& s, cudaStream_t stream) {
   if (dev >= 64) dev = 63;
   {
     std::lock_guard<std::mutex> lock(g_mu);
-    if (!g_ready[dev][kInPlace][kGran]) {
-      e = cudaFuncSetAttribute(pipe_kernel<kInPlace, kGran>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (!g_ready[dev][kInPlace][kGran][kIL]) {
+      e = cudaFuncSetAttribute(pipe_kernel<kInPlace, kGran, kIL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kSmemBytes);
       if (e != cudaSuccess) return e;
       int n = 0;
       cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
       g_sms[dev] = n > 0 ? n : 148;
-      g_ready[dev][kInPlace][kGran] = true;
+      g_ready[dev][kInPlace][kGran][kIL] = true;
     }
   }
   const uint64_t vbeg = s.lo / 8, vend = (s.hi + 7) / 8;
@@ -193,21 +217,25 @@ cudaError_t launch_t(const Span& s, cudaStream_t stream) {
   uint64_t grid = static_cast<uint64_t>(g_sms[dev]) * kCtasPerSm;
   const uint64_t need = (nstages + kPWarps - 1) / kPWarps;  // at least one stage per warp
   if (need < grid) grid = need;
-  pipe_kernel<kInPlace, kGran><<<static_cast<unsigned>(grid), kPThreads, kSmemBytes, stream>>>(s);
+  pipe_kernel<kInPlace, kGran, kIL><<<static_cast<unsigned>(grid), kPThreads, kSmemBytes, stream>>>(s);
   note_launch();
   return cudaGetLastError();
 }
 
 }  // namespace pipe
 
-cudaError_t launch_pipe(const Span& s, cudaStream_t stream) {
-  if (s.in != s.out) return pipe::launch_t<false, 1>(s, stream);
+template <bool kIL>
+static cudaError_t launch_pipe_il(const Span& s, cudaStream_t stream) {
+  if (s.in != s.out) return pipe::launch_t<false, 1, kIL>(s, stream);
   switch (inplace_granularity()) {
-    case 1: return pipe::launch_t<true, 1>(s, stream);
-    case 4: return pipe::launch_t<true, 4>(s, stream);
-    case 8: return pipe::launch_t<true, 8>(s, stream);
-    default: return pipe::launch_t<true, 2>(s, stream);
+    case 1: return pipe::launch_t<true, 1, kIL>(s, stream);
+    case 4: return pipe::launch_t<true, 4, kIL>(s, stream);
+    default: return pipe::launch_t<true, 2, kIL>(s, stream);
   }
+}
+
+cudaError_t launch_pipe(const Span& s, cudaStream_t stream) {
+  return pipe::interleave() ? launch_pipe_il<true>(s, stream) : launch_pipe_il<false>(s, stream);
 }
 
 }  // namespace u16m
