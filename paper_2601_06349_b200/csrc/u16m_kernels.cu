@@ -406,13 +406,14 @@ uint64_t tiles_for(const Span& s) {
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-// Kernel family selection. Default ("auto"): copy / in-place run the
-// register-staged kernel (measured best for plain streams: 6.8 TB/s copy,
-// interior tiles on a lean path), the batched form runs the TMA-pipelined kernel
+// Kernel family selection. Default ("auto"): copy / in-place run the rolling
+// register-pipeline stream kernel (u16m_stream.cu; measured best: 6.9 TB/s
+// copy, config 1 in 133 us), the batched form runs the TMA-pipelined kernel
 // (its producer warp walks the offsets off the consumers' critical path).
-// U16M_KERNEL overrides for A/B runs: "tma" (TMA for everything), "general"
-// (the general register-staged kernel for everything).
-enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoiceStream = 3 };
+// U16M_KERNEL overrides for A/B runs (profiles/README.md has the numbers):
+// "tma" (TMA-pipelined for everything), "pipe" (per-warp cp.async rings for
+// whole copy / in-place jobs), "general" (the 4-vector general kernel).
+enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoicePipe = 3 };
 // (kChoiceGeneral and kChoiceAuto share the register-staged kernel for plain
 // streams; they differ for the batched form.)
 static int kernel_choice() {
@@ -420,7 +421,7 @@ static int kernel_choice() {
     const char* e = std::getenv("U16M_KERNEL");
     if (e && std::strcmp(e, "tma") == 0) return int(kChoiceTma);
     if (e && std::strcmp(e, "general") == 0) return int(kChoiceGeneral);
-    if (e && std::strcmp(e, "stream") == 0) return int(kChoiceStream);
+    if (e && std::strcmp(e, "pipe") == 0) return int(kChoicePipe);
     return int(kChoiceAuto);
   }();
   return choice;
@@ -454,8 +455,8 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
     if (part == kTilesInterior) return cudaSuccess;
     return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
   }
-  if ((in == out || same) && choice == kChoiceAuto && part == kTilesAll) return launch_pipe(s, stream);
-  if ((in == out || same) && (choice == kChoiceAuto || choice == kChoiceStream))
+  if ((in == out || same) && choice == kChoicePipe && part == kTilesAll) return launch_pipe(s, stream);
+  if ((in == out || same) && (choice == kChoiceAuto || choice == kChoicePipe))
     return launch_stream(s, part, stream);
   s.tile_sel = part;
   const uint64_t grid = part == kTilesAll ? ntiles
