@@ -69,8 +69,9 @@ def traffic_for(config: str):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(config)
-    except (OSError, ValueError):
+            v = json.load(f).get(config)
+        return int(v) if v is not None else None
+    except (OSError, ValueError, TypeError):
         return None
 
 
