@@ -38,6 +38,9 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
 // in-place jobs; `s` from make_span, part as in launch_repair_part.
 struct Span;
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream);
+// Batched form on persistent warps with the rolling register pipeline.
+cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
+                                  cudaStream_t stream);
 // Warp-pipelined cp.async kernel (u16m_pipe.cu): whole same-phase jobs.
 cudaError_t launch_pipe(const Span& s, cudaStream_t stream);
 

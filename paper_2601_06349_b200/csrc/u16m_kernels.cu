@@ -554,8 +554,9 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
 
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream) {
-  if (kernel_choice() != kChoiceGeneral && ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0)
-    return launch_batched_tma(in, offsets, num_strings, out, stream);
+  const bool same16 = ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
+  if (kernel_choice() == kChoiceTma && same16) return launch_batched_tma(in, offsets, num_strings, out, stream);
+  if (kernel_choice() == kChoiceAuto && same16) return launch_batched_stream(in, offsets, num_strings, out, stream);
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
   const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
