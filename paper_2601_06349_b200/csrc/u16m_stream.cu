@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "u16m_internal.h"
 #include "u16m_repair.cuh"
@@ -29,8 +30,10 @@ constexpr int kSThreads = 256;
 constexpr int kSWarpVecs = 32 * kSV;          // 256 vectors = 4 KiB per warp
 constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;  // 2048 vectors = 32 KiB per CTA
 
-template <bool kInPlace, int kGran>
-__global__ void __launch_bounds__(kSThreads, 4) stream_kernel(Span s) {
+template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4>
+__global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s) {
+  constexpr int kSWarpVecs = 32 * kSV;
+  constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
   const int lane = threadIdx.x & 31;
   const uint32_t lane_off = threadIdx.x / 32 * kSWarpVecs + lane;
   const uint64_t vbeg = s.lo / 8;
@@ -294,29 +297,48 @@ cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, si
   return cudaGetLastError();
 }
 
-cudaError_t launch_stream(const Span& s0, int part, cudaStream_t stream) {
-  Span s = s0;
+// Vectors per thread of the stream kernel (U16M_STREAM_VECS: 8, 12 or 16;
+// A/B knob — register-staged bytes in flight per SM vs occupancy).
+static int stream_vecs() {
+  static const int v = [] {
+    const char* e = std::getenv("U16M_STREAM_VECS");
+    const int x = e ? std::atoi(e) : kDefaultStreamVecs;
+    return (x == 8 || x == 12 || x == 16) ? x : kDefaultStreamVecs;
+  }();
+  return v;
+}
+
+template <int kV, int kMB>
+static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
+  constexpr int kCtaVecs = (kSThreads / 32) * 32 * kV;
   const uint64_t vbeg = s.lo / 8, vend = (s.hi + 7) / 8;
-  const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
+  const uint64_t ntiles = (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
   uint64_t grid = ntiles;
   if (part == kTilesEdges) grid = ntiles < 2 ? ntiles : 2;
   if (part == kTilesInterior) grid = ntiles > 2 ? ntiles - 2 : 0;
   s.tile_sel = part;
   if (grid == 0) return cudaSuccess;
   const unsigned g = static_cast<unsigned>(grid);
-  const bool in_place = s.in == s.out;
-  if (!in_place) {
-    stream_kernel<false, 1><<<g, kSThreads, 0, stream>>>(s);
+  if (s.in != s.out) {
+    stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s);
   } else {
     switch (inplace_granularity()) {
-      case 1: stream_kernel<true, 1><<<g, kSThreads, 0, stream>>>(s); break;
-      case 4: stream_kernel<true, 4><<<g, kSThreads, 0, stream>>>(s); break;
-      case 8: stream_kernel<true, 8><<<g, kSThreads, 0, stream>>>(s); break;
-      default: stream_kernel<true, 2><<<g, kSThreads, 0, stream>>>(s); break;
+      case 1: stream_kernel<true, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s); break;
+      case 4: stream_kernel<true, 4, kV, kMB><<<g, kSThreads, 0, stream>>>(s); break;
+      case 8: stream_kernel<true, 8, kV, kMB><<<g, kSThreads, 0, stream>>>(s); break;
+      default: stream_kernel<true, 2, kV, kMB><<<g, kSThreads, 0, stream>>>(s); break;
     }
   }
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream) {
+  switch (stream_vecs()) {
+    case 12: return launch_stream_v<12, 3>(s, part, stream);
+    case 16: return launch_stream_v<16, 2>(s, part, stream);
+    default: return launch_stream_v<8, 4>(s, part, stream);
+  }
 }
 
 }  // namespace u16m
