@@ -117,6 +117,28 @@ u16m_status u16m_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
                                   unsigned long long* offsets_out,
                                   unsigned long long* count_out, void* stream);
 
+/* §8(f-3) codec fusion — replaces the decode -> to_well_formed -> replacement
+ * count -> encode sequence of the CLI's `fix` (proj/tools/main.cpp:62-89,
+ * codec.hpp:21-35): repairs n UTF-16 units stored as raw bytes in the given
+ * byte order (U16M_LITTLE_ENDIAN / U16M_BIG_ENDIAN) without a separate swap
+ * pass, writing the same byte order, and ADDS the number of replaced units to
+ * *replacements (device uint64; NULL = don't count). in/out: device, equal
+ * (in place) or disjoint with the same 16-byte alignment phase. Async. A BOM
+ * (FEFF) is an ordinary non-surrogate unit and may stay in the buffer. */
+#define U16M_LITTLE_ENDIAN 0
+#define U16M_BIG_ENDIAN 1
+u16m_status u16m_fix_utf16_bytes(const void* in, size_t n_units, void* out, int byte_order,
+                                 unsigned long long* replacements, void* stream);
+
+/* Host-memory forms (synchronous, staged through the GPU): the codec-fused
+ * repair with the replacement count returned in *replacements (host, may be
+ * NULL), and unpaired_surrogate_offsets for host buffers (units in host
+ * order; up to `limit` offsets, number written in *count_out). */
+u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out, int byte_order,
+                                      unsigned long long* replacements);
+u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,
+                                       unsigned long long* offsets_out, size_t* count_out);
+
 const char* u16m_status_string(u16m_status status);
 const char* u16m_last_error(void);
 int u16m_api_version(void);

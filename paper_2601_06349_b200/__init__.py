@@ -25,6 +25,7 @@ from ._lib import (  # noqa: F401
     count_unpaired,
     default_kernel,
     fix_str,
+    fix_utf16_bytes,
     fix_utf16le,
     generate_utf16le,
     is_well_formed_str,
@@ -34,6 +35,7 @@ from ._lib import (  # noqa: F401
     to_well_formed,
     to_well_formed_,
     to_well_formed_batched,
+    to_well_formed_bytes,
     to_well_formed_halo,
     to_well_formed_part,
     to_well_formed_sharded,
@@ -46,6 +48,8 @@ __all__ = [
     "default_kernel",
     "fix_str",
     "fix_utf16le",
+    "fix_utf16_bytes",
+    "to_well_formed_bytes",
     "generate_utf16le",
     "is_well_formed_str",
     "is_well_formed_utf16le",

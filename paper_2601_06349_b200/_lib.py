@@ -50,11 +50,15 @@ _L.u16m_gen_c3_offsets.argtypes = [ctypes.c_uint64, _sz, _vp, ctypes.POINTER(cty
 _L.u16m_gen_c3_content.argtypes = [ctypes.c_uint64, _sz, _vp, _u16p, _vp]
 _L.u16m_generate_reference_mix.argtypes = [_sz, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, _u16p]
 _L.u16m_l2_flush.argtypes = [_vp, _sz, _vp]
+_L.u16m_fix_utf16_bytes.argtypes = [_vp, _sz, _vp, ctypes.c_int, _vp, _vp]
+_L.u16m_fix_utf16_bytes_host.argtypes = [_vp, _sz, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong)]
+_L.u16m_unpaired_offsets_host.argtypes = [_vp, _sz, _sz, _vp, ctypes.POINTER(ctypes.c_size_t)]
 for _f in ("u16m_to_well_formed", "u16m_to_well_formed_in_place", "u16m_to_well_formed_batched",
            "u16m_to_well_formed_halo", "u16m_to_well_formed_halo_ptr", "u16m_to_well_formed_sharded",
            "u16m_to_well_formed_host", "u16m_to_well_formed_part", "u16m_count_unpaired", "u16m_unpaired_offsets",
            "u16m_gen_config", "u16m_gen_c3_offsets", "u16m_gen_c3_content",
-           "u16m_generate_reference_mix", "u16m_l2_flush"):
+           "u16m_generate_reference_mix", "u16m_l2_flush", "u16m_fix_utf16_bytes",
+           "u16m_fix_utf16_bytes_host", "u16m_unpaired_offsets_host"):
     getattr(_L, _f).restype = _st
 
 OK, INVALID, ALIAS, NOT_DEVICE, CUDA, MISALIGNED, NO_DEVICE = range(7)
@@ -294,6 +298,39 @@ def generate_utf16le(units: int, pair_pct: float = 0.0, mismatch_pct: float = 0.
     buf = (ctypes.c_char * len(out)).from_buffer(out)
     _check(_L.u16m_generate_reference_mix(units, pair_pct, mismatch_pct, seed, ctypes.addressof(buf)))
     return bytes(out)
+
+
+def fix_utf16_bytes(data, byte_order: str = "le") -> tuple[bytes, int]:
+    """§8(f-3) codec fusion: repair raw UTF-16 bytes in their own byte order
+    ("le" / "be") on the GPU without a swap pass; returns (bytes, number of
+    replaced units). The CLI `fix` path (paper_2601_06349_b200/u16m)."""
+    mv = _check_bytes(data)
+    if byte_order not in ("le", "be"):
+        raise ValueError("byte_order must be 'le' or 'be'")
+    out = bytearray(mv.nbytes)
+    n = mv.nbytes // 2
+    if n == 0:
+        return bytes(out), 0
+    src = bytearray(mv)
+    a = (ctypes.c_char * len(src)).from_buffer(src)
+    b = (ctypes.c_char * len(out)).from_buffer(out)
+    cnt = ctypes.c_ulonglong(0)
+    _check(_L.u16m_fix_utf16_bytes_host(ctypes.addressof(a), n, ctypes.addressof(b), 1 if byte_order == "be" else 0,
+                                        ctypes.byref(cnt)))
+    return bytes(out), int(cnt.value)
+
+
+def to_well_formed_bytes(x: torch.Tensor, out: Optional[torch.Tensor] = None, big_endian: bool = False,
+                         count: bool = False, stream=None):
+    """Device form of fix_utf16_bytes: x holds units as raw int16 words in the
+    given byte order. Returns out, or (out, replacements) when count=True."""
+    _units(x, "x")
+    out = torch.empty_like(x) if out is None else _units(out, "out")
+    cnt = torch.zeros(1, dtype=torch.int64, device=x.device) if count else None
+    with torch.cuda.device(x.device):
+        _check(_L.u16m_fix_utf16_bytes(x.data_ptr(), x.numel(), out.data_ptr(), 1 if big_endian else 0,
+                                       cnt.data_ptr() if cnt is not None else None, _stream(x, stream)))
+    return (out, int(cnt.item())) if count else out
 
 
 def available_kernels() -> list[str]:

@@ -103,6 +103,7 @@ size_t pipe_chunk_units() {
 struct HostPipe {
   int device = -1;
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  unsigned long long* counter = nullptr;  // device replacement counter (codec jobs)
   uint16_t* dbuf[kRing] = {};
   cudaEvent_t loaded[kRing] = {}, repaired[kRing] = {}, drained[kRing] = {};
 };
@@ -118,6 +119,7 @@ HostPipe* pipe_for(int device, u16m_status* st) {
   cudaError_t e = cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&p->counter, sizeof(unsigned long long));
   for (int i = 0; i < kRing && e == cudaSuccess; i++) {
     e = cudaMalloc(&p->dbuf[i], kChunkUnits * sizeof(uint16_t));
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->loaded[i], cudaEventDisableTiming);
@@ -244,6 +246,25 @@ u16m_status u16m_to_well_formed_batched(const uint16_t* in, const int64_t* offse
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "batched repair kernel launch");
 }
 
+u16m_status u16m_fix_utf16_bytes(const void* in, size_t n_units, void* out, int byte_order,
+                                 unsigned long long* replacements, void* stream) {
+  if (byte_order != U16M_LITTLE_ENDIAN && byte_order != U16M_BIG_ENDIAN)
+    return fail(U16M_ERR_INVALID_ARGUMENT, "byte_order must be U16M_LITTLE_ENDIAN or U16M_BIG_ENDIAN");
+  const auto* i = static_cast<const uint16_t*>(in);
+  auto* o = static_cast<uint16_t*>(out);
+  U16M_TRY(check_pair(i, n_units, o));
+  if (n_units == 0) return U16M_OK;
+  if (i != o && ((reinterpret_cast<uintptr_t>(i) ^ reinterpret_cast<uintptr_t>(o)) & 15u))
+    return fail(U16M_ERR_MISALIGNED, "byte-order-aware repair needs in/out with the same 16-byte phase");
+  U16M_TRY(check_device_present());
+  U16M_TRY(check_device_ptr(in, "in"));
+  if (o != i) U16M_TRY(check_device_ptr(out, "out"));
+  if (replacements) U16M_TRY(check_device_ptr(replacements, "replacements"));
+  const cudaError_t e = u16m::launch_fix_bytes(in, n_units, out, byte_order == U16M_BIG_ENDIAN, replacements,
+                                              as_stream(stream), -1, -1);
+  return e == cudaSuccess ? U16M_OK : cuda_fail(e, "codec repair kernel launch");
+}
+
 u16m_status u16m_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
                                 void* stream) {
   if (count_out == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "count_out is null");
@@ -272,8 +293,13 @@ u16m_status u16m_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "offsets kernels");
 }
 
-u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out) {
+// Shared body of the host-memory entry points. byte_order < 0: plain repair
+// (units in host order); 0/1: codec-fused repair in LE/BE byte order with an
+// optional replacement count (host pointer).
+static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, int byte_order,
+                                 unsigned long long* replacements) {
   U16M_TRY(check_pair(in, n, out));
+  if (replacements) *replacements = 0;
   if (n == 0) return U16M_OK;
   U16M_TRY(check_device_present());
   int dev = 0;
@@ -283,6 +309,15 @@ u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out
   u16m_status st = U16M_OK;
   HostPipe* p = pipe_for(dev, &st);
   if (p == nullptr) return st;
+  const bool be = byte_order == U16M_BIG_ENDIAN;
+  auto unit = [&](size_t i) -> int32_t {  // unit value of in[i] in the job's byte order
+    const uint32_t w = in[i];
+    return static_cast<int32_t>(be ? (((w & 0xFFu) << 8) | (w >> 8)) : w);
+  };
+  if (replacements) {
+    e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
+    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+  }
   size_t c = 0;
   const size_t chunk = pipe_chunk_units();
   for (size_t c0 = 0; c0 < n; c0 += chunk, c++) {
@@ -291,8 +326,8 @@ u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out
     // Halo units are read from the host copy at enqueue time. For in-place
     // jobs an earlier chunk's D2H may already have rewritten in[c0-1]; that
     // is benign (a unit is only rewritten when no neighbour pairs with it).
-    const int32_t left = c0 > 0 ? static_cast<int32_t>(in[c0 - 1]) : -1;
-    const int32_t right = c0 + len < n ? static_cast<int32_t>(in[c0 + len]) : -1;
+    const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
+    const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
     if (c >= static_cast<size_t>(kRing)) {
       e = cudaStreamWaitEvent(p->h2d, p->drained[k], 0);
       if (e != cudaSuccess) return cuda_fail(e, "pipeline wait");
@@ -301,7 +336,11 @@ u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
     cudaEventRecord(p->loaded[k], p->h2d);
     cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-    e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, p->comp);
+    if (byte_order < 0)
+      e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, p->comp);
+    else
+      e = u16m::launch_fix_bytes(p->dbuf[k], len, p->dbuf[k], be, replacements ? p->counter : nullptr, p->comp,
+                                 left, right);
     if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
     cudaEventRecord(p->repaired[k], p->comp);
     cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
@@ -312,7 +351,48 @@ u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out
   e = cudaStreamSynchronize(p->d2h);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->h2d);
+  if (e == cudaSuccess && replacements)
+    e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "host pipeline sync");
+  return U16M_OK;
+}
+
+u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out) {
+  return host_pipeline(in, n, out, -1, nullptr);
+}
+
+u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out, int byte_order,
+                                      unsigned long long* replacements) {
+  if (byte_order != U16M_LITTLE_ENDIAN && byte_order != U16M_BIG_ENDIAN)
+    return fail(U16M_ERR_INVALID_ARGUMENT, "byte_order must be U16M_LITTLE_ENDIAN or U16M_BIG_ENDIAN");
+  return host_pipeline(static_cast<const uint16_t*>(in), n_units, static_cast<uint16_t*>(out), byte_order,
+                       replacements);
+}
+
+u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,
+                                       unsigned long long* offsets_out, size_t* count_out) {
+  if (count_out == nullptr || (limit > 0 && offsets_out == nullptr))
+    return fail(U16M_ERR_INVALID_ARGUMENT, "null output");
+  *count_out = 0;
+  if (n == 0 || limit == 0) return U16M_OK;
+  if (in == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "null buffer with n > 0");
+  U16M_TRY(check_device_present());
+  if (limit > n) limit = n;
+  void* ws = nullptr;
+  const size_t bytes = n * 2 + limit * 8 + 64;
+  cudaError_t e = cudaMalloc(&ws, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "workspace");
+  auto* d_off = static_cast<unsigned long long*>(ws);
+  auto* d_cnt = d_off + limit;
+  auto* d_in = reinterpret_cast<uint16_t*>(d_cnt + 4);
+  e = cudaMemcpy(d_in, in, n * 2, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = u16m::launch_unpaired_offsets(d_in, n, limit, d_off, d_cnt, nullptr);
+  unsigned long long cnt = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && cnt) e = cudaMemcpy(offsets_out, d_off, cnt * 8, cudaMemcpyDeviceToHost);
+  cudaFree(ws);
+  if (e != cudaSuccess) return cuda_fail(e, "unpaired offsets");
+  *count_out = static_cast<size_t>(cnt);
   return U16M_OK;
 }
 

@@ -39,11 +39,19 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
 // in-place jobs; `s` from make_span, part as in launch_repair_part.
 struct Span;
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream);
+// Codec-fused form (u16m_stream.cu): same-phase buffers in little- or
+// big-endian byte order, optional device replacement counter (accumulated).
+cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long long* count, cudaStream_t stream);
 // Batched form on persistent warps with the rolling register pipeline.
 cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
                                   cudaStream_t stream);
 // Warp-pipelined cp.async kernel (u16m_pipe.cu): whole same-phase jobs.
 cudaError_t launch_pipe(const Span& s, cudaStream_t stream);
+
+// §8(f-3): byte-order-aware repair + replacement count (same 16-byte phase).
+// left/right: halo UNIT values (byte order already resolved), -1 = outside.
+cudaError_t launch_fix_bytes(const void* in, size_t n, void* out, bool big_endian, unsigned long long* count,
+                             cudaStream_t stream, int32_t left, int32_t right);
 
 cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
                                   cudaStream_t stream);

@@ -89,18 +89,6 @@ __device__ __forceinline__ uint64_t warp_lower_bound(const int64_t* off, uint64_
   return m ? lo + (__ffs(m) - 1) : hi;
 }
 
-// Clear the flags of units outside [lo, hi) (edge vectors only).
-__device__ __forceinline__ void mask_outside(const Span& s, uint64_t vi, uint32_t& B0, uint32_t& B1) {
-#pragma unroll
-  for (int j = 0; j < 8; j++) {
-    const uint64_t a = vi * 8 + j;
-    if (a < s.lo || a >= s.hi) {
-      if (j < 4) B0 &= ~(0x80u << (8 * j));
-      else B1 &= ~(0x80u << (8 * (j - 4)));
-    }
-  }
-}
-
 // Marks every string start of this CTA tile in `starts` (bit i = aligned unit
 // cta_v0*8 + i). Warp 0 searches; the CTA synchronises around it.
 __device__ __forceinline__ void mark_string_starts(const BatchArgs& b, uint64_t cta_v0, uint32_t* starts,
@@ -472,6 +460,17 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
   }
   if (same) return launch<kCopy, true, false>(s, kNoBatch, kNoScan, grid, stream);
   return launch<kCopy, false, false>(s, kNoBatch, kNoScan, grid, stream);
+}
+
+cudaError_t launch_fix_bytes(const void* in, size_t n, void* out, bool big_endian, unsigned long long* count,
+                             cudaStream_t stream, int32_t left, int32_t right) {
+  if (n == 0) return cudaSuccess;
+  bool same = false;
+  const auto* i16 = static_cast<const uint16_t*>(in);
+  auto* o16 = static_cast<uint16_t*>(out);
+  const Span s = make_span(i16, n, o16, left, right, nullptr, nullptr, &same);
+  if (!(i16 == o16 || same)) return cudaErrorInvalidValue;
+  return launch_stream_codec(s, big_endian, count, stream);
 }
 
 cudaError_t launch_repair(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,

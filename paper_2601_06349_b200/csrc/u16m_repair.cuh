@@ -78,16 +78,41 @@ __device__ __forceinline__ void classify4(uint32_t wa, uint32_t wb, uint32_t& H,
   L = sur & b10;
 }
 
+// Big-endian byte order (§8(f-3) codec fusion): the high byte of each unit
+// is the FIRST byte in memory, so only the byte-gather selector changes; the
+// vector stays in memory order end to end.
+__device__ __forceinline__ void classify4_be(uint32_t wa, uint32_t wb, uint32_t& H, uint32_t& L) {
+  const uint32_t hb = prmt(wa, wb, 0x6420);
+  const uint32_t s = (hb & 0xF8F8F8F8u) ^ 0xD8D8D8D8u;
+  const uint32_t t = (s >> 1) + 0x7C7C7C7Cu;
+  const uint32_t sur = ~t & 0x80808080u;
+  const uint32_t b10 = hb << 5;
+  H = sur & ~b10;
+  L = sur & b10;
+}
+
 // Flags of one vector: units 0-3 in (H0,L0), units 4-7 in (H1,L1).
 struct Flags {
   uint32_t H0, L0, H1, L1;
 };
 
+template <bool kBE = false>
 __device__ __forceinline__ Flags classify8(const uint4& v) {
   Flags f;
-  classify4(v.x, v.y, f.H0, f.L0);
-  classify4(v.z, v.w, f.H1, f.L1);
+  if constexpr (kBE) {
+    classify4_be(v.x, v.y, f.H0, f.L0);
+    classify4_be(v.z, v.w, f.H1, f.L1);
+  } else {
+    classify4(v.x, v.y, f.H0, f.L0);
+    classify4(v.z, v.w, f.H1, f.L1);
+  }
   return f;
+}
+
+// Unit value <-> its 16-bit memory word in the given byte order.
+template <bool kBE>
+__device__ __forceinline__ uint32_t to_mem(uint32_t u) {
+  return kBE ? (((u & 0xFFu) << 8) | ((u >> 8) & 0xFFu)) : u;
 }
 
 // Bad-unit flags. hp: byte lane 3 holds H(unit before unit 0); ln: byte lane
@@ -110,17 +135,20 @@ __device__ __forceinline__ void bad8(const Flags& f, uint32_t hp, uint32_t ln, u
 }
 
 // Replace every flagged unit with U+FFFD. prmt selector nibbles 8..B copy
-// byte 0..3 with its sign bit replicated -> 0xFF / 0x00 byte masks.
+// byte 0..3 with its sign bit replicated -> 0xFF / 0x00 byte masks. U+FFFD in
+// memory order is FD FF (LE) or FF FD (BE).
+template <bool kBE = false>
 __device__ __forceinline__ uint4 blend(uint4 v, uint32_t B0, uint32_t B1) {
+  constexpr uint32_t R = kBE ? 0xFDFFFDFFu : 0xFFFDFFFDu;
   uint32_t m;
   m = prmt(B0, 0, 0x9988);
-  v.x = (v.x & ~m) | (0xFFFDFFFDu & m);
+  v.x = (v.x & ~m) | (R & m);
   m = prmt(B0, 0, 0xBBAA);
-  v.y = (v.y & ~m) | (0xFFFDFFFDu & m);
+  v.y = (v.y & ~m) | (R & m);
   m = prmt(B1, 0, 0x9988);
-  v.z = (v.z & ~m) | (0xFFFDFFFDu & m);
+  v.z = (v.z & ~m) | (R & m);
   m = prmt(B1, 0, 0xBBAA);
-  v.w = (v.w & ~m) | (0xFFFDFFFDu & m);
+  v.w = (v.w & ~m) | (R & m);
   return v;
 }
 
@@ -150,11 +178,25 @@ __device__ __forceinline__ void set_unit(uint4& v, int j, uint32_t u) {
   *w = (j & 1) ? ((*w & 0x0000FFFFu) | (u << 16)) : ((*w & 0xFFFF0000u) | (u & 0xFFFFu));
 }
 
-// Vector vi straddles or lies outside [lo, hi): substitute out-of-range units.
+// Vector vi straddles or lies outside [lo, hi): substitute out-of-range units
+// (halo values are unit values; the vector is in memory byte order).
+template <bool kBE = false>
 __device__ __forceinline__ void patch_edges(const Span& s, uint64_t vi, uint4& v) {
   for (int j = 0; j < 8; j++) {
     const uint64_t a = vi * 8 + j;
-    if (a < s.lo || a >= s.hi) set_unit(v, j, unit_at(s, static_cast<int64_t>(a)));
+    if (a < s.lo || a >= s.hi) set_unit(v, j, to_mem<kBE>(unit_at(s, static_cast<int64_t>(a))));
+  }
+}
+
+// Clear the flags of units outside [lo, hi) (edge vectors; counting).
+__device__ __forceinline__ void mask_outside(const Span& s, uint64_t vi, uint32_t& B0, uint32_t& B1) {
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const uint64_t a = vi * 8 + j;
+    if (a < s.lo || a >= s.hi) {
+      if (j < 4) B0 &= ~(0x80u << (8 * j));
+      else B1 &= ~(0x80u << (8 * (j - 4)));
+    }
   }
 }
 

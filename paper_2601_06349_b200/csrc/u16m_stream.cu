@@ -30,8 +30,11 @@ constexpr int kSThreads = 256;
 constexpr int kSWarpVecs = 32 * kSV;          // 256 vectors = 4 KiB per warp
 constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;  // 2048 vectors = 32 KiB per CTA
 
-template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4>
-__global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s) {
+// kBE: units are big-endian in memory (fused byte-order handling, §8(f-3));
+// kCount: add the number of rewritten units to *count (warp reduction, one
+// atomic per warp).
+template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false>
+__global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count) {
   constexpr int kSWarpVecs = 32 * kSV;
   constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
   const int lane = threadIdx.x & 31;
@@ -53,33 +56,43 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s) {
 #pragma unroll
     for (int k = 0; k < kSV; k++) v[k] = ld_stream(src + k * 32);
     const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
-    if (lane == 0) halo = src16[-1];
-    if (lane == 31) halo = src16[(kSV - 1) * 32 * 8 + 8];
+    if (lane == 0) halo = to_mem<kBE>(src16[-1]);
+    if (lane == 31) halo = to_mem<kBE>(src16[(kSV - 1) * 32 * 8 + 8]);
   } else {
 #pragma unroll
     for (int k = 0; k < kSV; k++) {
       const uint64_t vi = v0 + k * 32;
       v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
     }
+    // unit_at returns unit values for halos but raw memory words in range.
     const uint64_t warp_v0 = v0 - lane;
-    if (lane == 0) halo = unit_at(s, static_cast<int64_t>(warp_v0 * 8) - 1);
-    if (lane == 31) halo = unit_at(s, static_cast<int64_t>((warp_v0 + kSWarpVecs) * 8));
+    if (lane == 0) {
+      const int64_t a = static_cast<int64_t>(warp_v0 * 8) - 1;
+      halo = unit_at(s, a);
+      if (a >= static_cast<int64_t>(s.lo)) halo = to_mem<kBE>(halo);
+    }
+    if (lane == 31) {
+      const int64_t a = static_cast<int64_t>((warp_v0 + kSWarpVecs) * 8);
+      halo = unit_at(s, a);
+      if (a < static_cast<int64_t>(s.hi)) halo = to_mem<kBE>(halo);
+    }
 #pragma unroll
     for (int k = 0; k < kSV; k++) {
       const uint64_t vi = v0 + k * 32;
-      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, v[k]);
+      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges<kBE>(s, vi, v[k]);
     }
   }
+  uint32_t counted = 0;
 
   // Rolling pipeline over k: flags of vector k (cur) and k+1 (nxt) live.
-  Flags cur = classify8(v[0]);
+  Flags cur = classify8<kBE>(v[0]);
   uint32_t hp_carry = hflag_hi(halo);  // lane 0: H flags of the unit before vector 0
   const uint32_t halo_l = lflag_lo(halo);
   uint4* dst = s.out + v0;
 #pragma unroll
   for (int k = 0; k < kSV; k++) {
     Flags nxt;
-    if (k + 1 < kSV) nxt = classify8(v[k + 1]);
+    if (k + 1 < kSV) nxt = classify8<kBE>(v[k + 1]);
     const uint32_t up = __shfl_sync(kFull, cur.H1, (lane + 31) & 31);  // lane 0 gets lane 31's (vector k)
     const uint32_t dn = __shfl_sync(kFull, cur.L0, (lane + 1) & 31);
     uint32_t ln = dn;
@@ -95,10 +108,15 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s) {
     bad8(cur, hp, ln, B0, B1);
     const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
     const uint64_t vi = v0 + k * 32;
+    if constexpr (kCount) {
+      uint32_t c0 = B0, c1 = B1;
+      if (!interior) mask_outside(s, vi, c0, c1);
+      if (vi < vend) counted += __popc(c0) + __popc(c1);
+    }
     if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
-      if (store) st_stream(dst + k * 32, blend(v[k], B0, B1));
+      if (store) st_stream(dst + k * 32, blend<kBE>(v[k], B0, B1));
     } else if (store && vi < vend) {
-      const uint4 r = blend(v[k], B0, B1);
+      const uint4 r = blend<kBE>(v[k], B0, B1);
 #pragma unroll
       for (int j = 0; j < 8; j++) {
         const uint64_t a = vi * 8 + j;
@@ -109,6 +127,11 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s) {
       }
     }
     if (k + 1 < kSV) cur = nxt;
+  }
+  if constexpr (kCount) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) counted += __shfl_xor_sync(kFull, counted, o);
+    if (lane == 0 && counted) atomicAdd(count, static_cast<unsigned long long>(counted));
   }
 }
 
@@ -320,15 +343,41 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
   if (grid == 0) return cudaSuccess;
   const unsigned g = static_cast<unsigned>(grid);
   if (s.in != s.out) {
-    stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s);
+    stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr);
   } else {
     switch (inplace_granularity()) {
-      case 1: stream_kernel<true, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s); break;
-      case 4: stream_kernel<true, 4, kV, kMB><<<g, kSThreads, 0, stream>>>(s); break;
-      case 8: stream_kernel<true, 8, kV, kMB><<<g, kSThreads, 0, stream>>>(s); break;
-      default: stream_kernel<true, 2, kV, kMB><<<g, kSThreads, 0, stream>>>(s); break;
+      case 1: stream_kernel<true, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr); break;
+      case 4: stream_kernel<true, 4, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr); break;
+      case 8: stream_kernel<true, 8, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr); break;
+      default: stream_kernel<true, 2, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr); break;
     }
   }
+  note_launch();
+  return cudaGetLastError();
+}
+
+// Byte-order-aware repair with a replacement count (codec fusion, §8(f-3)).
+template <bool kInPlace, bool kBE>
+static void launch_codec_t(const Span& s, unsigned g, unsigned long long* count, cudaStream_t stream) {
+  if (count)
+    stream_kernel<kInPlace, 2, 8, 4, kBE, true><<<g, kSThreads, 0, stream>>>(s, count);
+  else
+    stream_kernel<kInPlace, 2, 8, 4, kBE, false><<<g, kSThreads, 0, stream>>>(s, nullptr);
+}
+
+cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long long* count, cudaStream_t stream) {
+  constexpr int kCtaVecs = (kSThreads / 32) * 32 * 8;
+  const uint64_t vbeg = s.lo / 8, vend = (s.hi + 7) / 8;
+  const uint64_t ntiles = (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
+  if (ntiles == 0) return cudaSuccess;
+  Span t = s;
+  t.tile_sel = kTilesAll;
+  const unsigned g = static_cast<unsigned>(ntiles);
+  const bool ip = s.in == s.out;
+  if (ip && big_endian) launch_codec_t<true, true>(t, g, count, stream);
+  else if (ip) launch_codec_t<true, false>(t, g, count, stream);
+  else if (big_endian) launch_codec_t<false, true>(t, g, count, stream);
+  else launch_codec_t<false, false>(t, g, count, stream);
   note_launch();
   return cudaGetLastError();
 }

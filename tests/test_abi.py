@@ -101,3 +101,16 @@ def test_generate_utf16le_matches_reference_generator():
 def test_header_is_plain_c():
     text = open(os.path.join(INC, "u16m.h")).read()
     assert "torch" not in text and "cuda_runtime" not in text and "extern \"C\"" in text
+
+
+def test_cli_usage_errors_without_gpu(tmp_path):
+    cli = os.path.join(LIBDIR, "u16m")
+    assert os.path.exists(cli)
+    assert subprocess.run([cli], capture_output=True).returncode == 2
+    assert subprocess.run([cli, "bogus"], capture_output=True).returncode == 2
+    f = tmp_path / "x"
+    f.write_bytes(b"\x41\x00")
+    p = subprocess.run([cli, "fix", str(f)], capture_output=True, text=True)
+    assert p.returncode == 2 and "--in-place or --output" in p.stderr
+    p = subprocess.run([cli, "fix", "-k", "warp9", str(f), "-o", str(f) + ".o"], capture_output=True, text=True)
+    assert p.returncode == 2 and "unknown kernel" in p.stderr
