@@ -275,7 +275,8 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    distributed = world > 1 or args.force_dist
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
     L = _lib.raw()
     cfg, per_gpu, mode, seed, desc = CONFIGS[args.config]
@@ -302,7 +303,7 @@ def run_ours(args):
         if mode == "batched":
             _lib._check(L.u16m_to_well_formed_batched(data.data_ptr(), offsets.data_ptr(), offsets.numel() - 1,
                                                      out.data_ptr(), sptr))
-        elif world > 1:
+        elif distributed:
             pdist.repair_shard(data, out)
         elif mode == "inplace":
             _lib._check(L.u16m_to_well_formed_in_place(data.data_ptr(), units, sptr))
@@ -320,7 +321,7 @@ def run_ours(args):
         prepare()
         step_kernel()
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = P.launch_count()
@@ -335,14 +336,14 @@ def run_ours(args):
             repair_launches += P.launch_count() - c0
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if distributed:
             dist.barrier()
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_local = sum(step_ms) / 1e3
     t = torch.tensor([t_local], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     all_launches = P.launch_count() - launches0
@@ -370,7 +371,7 @@ def run_ours(args):
         for i in range(args.warmup + e2e_steps):
             if hsrc is not None:
                 hin.copy_(hsrc)
-            if world > 1:
+            if distributed:
                 dist.barrier()
             t0 = time.perf_counter()
             _lib._check(L.u16m_to_well_formed_host(hin.data_ptr(), units, hout.data_ptr()))
@@ -378,7 +379,7 @@ def run_ours(args):
             if i >= args.warmup:
                 times.append(dt)
         te = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
-        if world > 1:
+        if distributed:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(world * in_bytes * len(times) / float(te.item()) / 1e9, 3), "unit": UNIT,
                "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": in_bytes,
@@ -398,7 +399,7 @@ def run_ours(args):
         except Exception as e:  # noqa: BLE001
             log("cpu baseline failed:", e)
 
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
     if rank != 0:
@@ -417,7 +418,7 @@ def run_ours(args):
         "dtype": "u16",
         "data": "synthetic",
         "config": {"workload": desc, "units_per_gpu": units, "mode": mode,
-                   "parallelism": f"shard{world}" if world > 1 else "single",
+                   "parallelism": f"shard{world}" if distributed else "single",
                    "l2": "flushed before every step (512 MiB streaming read) + restore outside the event pair",
                    "hbm_fraction_of_measured_peak": round((value / world) * (algo_bytes / in_bytes) / peak, 4),
                    "output_check_well_formed": bool(ok)},
@@ -433,7 +434,28 @@ def run_ours(args):
         "wall_s_timed_loop": round(wall, 4),
     }
     print(json.dumps(line), flush=True)
+    if args.csv:
+        write_csv(args.csv, [("cuda-sm100a" + (f"-x{world}" if world > 1 else ""), world * units, t_max / args.steps,
+                              None)] + ([("reference-" + cpu["kind"], None, None, cpu)] if cpu else []))
     return 0
+
+
+def write_csv(path, rows):
+    """Append rows in the reference's CSV schema (proj/src/bench.cpp:151-163):
+    impl,input_units,bytes,best_ns,mean_ns,gbps,error_margin_pct (decimal GB/s
+    of input bytes, 2 B per unit)."""
+    header = "impl,input_units,bytes,best_ns,mean_ns,gbps,error_margin_pct"
+    new = not os.path.exists(path)
+    with open(path, "a") as f:
+        if new:
+            f.write(header + "\n")
+        for impl, units, sec, cpu in rows:
+            if cpu is not None:
+                gbps = cpu["value"]
+                f.write(f"{impl},,,,,{gbps:.3f},\n")
+            else:
+                ns = sec * 1e9
+                f.write(f"{impl},{units},{2 * units},{ns:.0f},{ns:.0f},{2 * units / ns:.3f},0.000\n")
 
 
 def main():
@@ -445,6 +467,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the sharded (NCCL halo exchange) step even at N=1 (under torchrun)")
+    ap.add_argument("--csv", default=None,
+                    help="also append rows in the reference bench CSV schema (proj/src/bench.cpp:151-163)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
