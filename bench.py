@@ -277,7 +277,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     distributed = world > 1 or args.force_dist
     if distributed:
-        dist.init_process_group("nccl", device_id=dev)
+        pdist.init_process_group_for_repair("nccl", device_id=dev)
     L = _lib.raw()
     cfg, per_gpu, mode, seed, desc = CONFIGS[args.config]
     stream = torch.cuda.current_stream(dev)

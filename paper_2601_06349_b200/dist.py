@@ -80,9 +80,22 @@ _side_streams: dict = {}
 
 
 def _side_stream(device: torch.device) -> torch.cuda.Stream:
+    """High-priority side stream: the gather + edge tiles must be scheduled
+    ahead of the interior grid's pending CTAs, not after them."""
     if device not in _side_streams:
-        _side_streams[device] = torch.cuda.Stream(device=device)
+        lo, hi = torch.cuda.Stream.priority_range()
+        _side_streams[device] = torch.cuda.Stream(device=device, priority=hi)
     return _side_streams[device]
+
+
+def init_process_group_for_repair(backend: str = "nccl", **kw):
+    """init_process_group with NCCL on high-priority streams (the halo gather
+    then preempts the interior grid's queued CTAs instead of waiting for them)."""
+    if backend == "nccl":
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True
+        kw.setdefault("pg_options", opts)
+    dist.init_process_group(backend, **kw)
 
 
 def repair_shard(shard: torch.Tensor, out: Optional[torch.Tensor] = None, group=None, compute=None,
