@@ -381,6 +381,7 @@ Span make_span(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_
   s.left_ptr = left_ptr;
   s.right_ptr = right_ptr;
   s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
   *same_phase = out != nullptr && ((ia & 15u) == (oa & 15u));
   return s;
 }
@@ -554,8 +555,9 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream) {
   const bool same16 = ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
-  if (kernel_choice() == kChoiceTma && same16) return launch_batched_tma(in, offsets, num_strings, out, stream);
-  if (kernel_choice() == kChoiceAuto && same16) return launch_batched_stream(in, offsets, num_strings, out, stream);
+  if ((kernel_choice() == kChoiceTma || kernel_choice() == kChoiceAuto) && same16)
+    return launch_batched_tma(in, offsets, num_strings, out, stream);
+  if (kernel_choice() == kChoicePipe && same16) return launch_batched_stream(in, offsets, num_strings, out, stream);
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
   const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
@@ -567,6 +569,7 @@ cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t nu
   s.left = s.right = -1;
   s.left_ptr = s.right_ptr = nullptr;
   s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
   const BatchArgs b{offsets, static_cast<uint64_t>(num_strings) + 1, ph};
   // Persistent grid: the range is only known on the device.
   const uint64_t grid = static_cast<uint64_t>(sm_count_for_current_device()) * 8;

@@ -42,6 +42,7 @@ struct Span {
   const uint16_t* left_ptr;   // device-side halo (overrides left/right if set)
   const uint16_t* right_ptr;
   int tile_sel;            // kTilesAll / kTilesEdges / kTilesInterior
+  int prefetch_tiles;      // stream kernel: L2 bulk-prefetch distance in tiles (0 = off)
 };
 
 enum TileSel : int { kTilesAll = 0, kTilesEdges = 1, kTilesInterior = 2 };

@@ -51,6 +51,13 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
 
   uint4 v[kSV];
   uint32_t halo = 0;
+  if (s.prefetch_tiles > 0 && threadIdx.x == 0) {
+    // One bulk L2 prefetch of the tile a later wave of CTAs will stream: extra
+    // bytes in flight without registers (TMA prefetch, no smem, no barrier).
+    const uint64_t pv = tv0 + static_cast<uint64_t>(s.prefetch_tiles) * kSCtaVecs;
+    if (pv + kSCtaVecs <= vend)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s.in + pv), "r"(kSCtaVecs * 16) : "memory");
+  }
   if (interior) {
     const uint4* src = s.in + v0;
 #pragma unroll
@@ -303,6 +310,7 @@ cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, si
   s.left = s.right = -1;
   s.left_ptr = s.right_ptr = nullptr;
   s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = static_cast<unsigned>(sms * 3);
@@ -331,6 +339,14 @@ static int stream_vecs() {
   return v;
 }
 
+static int prefetch_setting() {
+  static const int v = [] {
+    const char* e = std::getenv("U16M_PREFETCH");
+    return e ? std::atoi(e) : -1;  // -1: auto (one resident wave ahead)
+  }();
+  return v;
+}
+
 template <int kV, int kMB>
 static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
   constexpr int kCtaVecs = (kSThreads / 32) * 32 * kV;
@@ -341,6 +357,12 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
   if (part == kTilesInterior) grid = ntiles > 2 ? ntiles - 2 : 0;
   s.tile_sel = part;
   if (grid == 0) return cudaSuccess;
+  {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int pf = prefetch_setting();
+    s.prefetch_tiles = pf < 0 ? sms * kMB : pf;
+  }
   const unsigned g = static_cast<unsigned>(grid);
   if (s.in != s.out) {
     stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr);

@@ -359,6 +359,7 @@ cudaError_t launch_repair_tma(const uint16_t* in, size_t n, uint16_t* out, int32
   s.left_ptr = left_ptr;
   s.right_ptr = right_ptr;
   s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
   const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kCtaVecs - 1) / kCtaVecs;
   const tma::BatchArgsT b{nullptr, 0, 0};
   if (in != out) return tma::launch_tma<0, false, 1>(s, b, ntiles, stream);
@@ -383,6 +384,7 @@ cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_
   s.left = s.right = -1;
   s.left_ptr = s.right_ptr = nullptr;
   s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
   const tma::BatchArgsT b{offsets, static_cast<uint64_t>(num_strings) + 1, ph};
   if (in == out) return tma::launch_tma<1, true, 1>(s, b, 0, stream);
   return tma::launch_tma<0, true, 1>(s, b, 0, stream);
