@@ -361,7 +361,9 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int pf = prefetch_setting();
-    s.prefetch_tiles = pf < 0 ? sms * kMB : pf;
+    // auto: one resident wave ahead, and only for jobs of more than two waves
+    // (measured: +3% on config 1, a small loss on the 2-wave config 0).
+    s.prefetch_tiles = pf >= 0 ? pf : (ntiles > static_cast<uint64_t>(2 * sms * kMB) ? sms * kMB : 0);
   }
   const unsigned g = static_cast<unsigned>(grid);
   if (s.in != s.out) {
