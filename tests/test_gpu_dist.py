@@ -1,0 +1,25 @@
+"""GPU + NCCL: the one-process-per-GPU sharded step (dist.repair_shard) under
+torchrun, checked against the CPU oracle (world size = visible GPUs, capped at
+2; one GPU here)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+HELPER = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gpu_helpers", "dist_check.py")
+
+
+def test_torchrun_sharded_step(cuda):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    n = min(torch.cuda.device_count(), 2)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), HELPER],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ALL OK" in r.stdout
