@@ -33,8 +33,9 @@ def main():
                 src = x.clone()
                 out = src if in_place else torch.empty_like(src)
                 pdist.repair_shard(src, out, overlap=overlap)
-                parts = [torch.empty_like(out) for _ in range(world)]
-                dist.all_gather(parts, out)
+                b = out.view(torch.uint8)  # NCCL has no 16-bit integer type
+                parts = [torch.empty_like(b) for _ in range(world)]
+                dist.all_gather(parts, b)
                 if rank == 0:
                     got = torch.cat(parts).cpu().numpy().view(np.uint16)
                     full = O.gen_config(cfg, total, seed=cfg, shard_len=per_rank if cfg == 4 else 0)
