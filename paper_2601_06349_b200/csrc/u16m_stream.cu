@@ -178,16 +178,8 @@ __device__ __forceinline__ uint64_t warp_lb(const int64_t* off, uint64_t count, 
   return m ? lo + (__ffs(m) - 1) : hi;
 }
 
-// One warp tile of the batched form: data, its offsets window (64 entries:
-// lane l holds w[0] = offsets[base + l], w[1] = offsets[base + 32 + l]).
-struct BTile {
-  uint4 v[kSV];
-  int64_t w[2];
-  uint64_t base;
-};
-
 template <bool kInPlace, int kGran>
-__global__ void __launch_bounds__(kSThreads, 2) batched_stream_kernel(Span s, const int64_t* __restrict__ offsets,
+__global__ void __launch_bounds__(kSThreads, 3) batched_stream_kernel(Span s, const int64_t* __restrict__ offsets,
                                                                       uint64_t count, uint32_t phase) {
   const int lane = threadIdx.x & 31;
   {
@@ -205,110 +197,77 @@ __global__ void __launch_bounds__(kSThreads, 2) batched_stream_kernel(Span s, co
   const uint64_t t0 = nwt * gw / nw, t1 = nwt * (gw + 1) / nw;
   if (t0 >= t1) return;
 
-  auto load_window = [&](BTile& b, uint64_t base) {
-    b.base = base;
-    b.w[0] = base + lane < count ? __ldg(offsets + base + lane) : INT64_MAX;
-    b.w[1] = base + 32 + lane < count ? __ldg(offsets + base + 32 + lane) : INT64_MAX;
-  };
-  auto load_data = [&](BTile& b, uint64_t t) {
-    const uint64_t v0 = vbeg + t * kSWarpVecs + lane;
-#pragma unroll
-    for (int k = 0; k < kSV; k++) {
-      const uint64_t vi = v0 + k * 32;
-      b.v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
-    }
-  };
-  // First string starting at or after aligned unit `a` (relative to b.base,
-  // when the window reaches that far; else -1).
-  auto first_at_or_after = [&](const BTile& b, int64_t key) -> int {
-    const uint32_t lt0 = __ballot_sync(kFull, b.w[0] < key);
-    const uint32_t lt1 = __ballot_sync(kFull, b.w[1] < key);
-    if (lt1 == kFull) return -1;  // window exhausted
-    return __popc(lt0) + __popc(lt1);
-  };
-
-  BTile cur, nxt;
+  // aligned unit a <-> absolute index a - phase
   uint64_t sidx = warp_lb(offsets, count, static_cast<int64_t>((vbeg + t0 * kSWarpVecs) * 8) - phase, lane);
-  load_data(cur, t0);
-  load_window(cur, sidx);
   uint32_t hp_carry = 0;
   if (lane == 0) hp_carry = hflag_hi(unit_at(s, static_cast<int64_t>((vbeg + t0 * kSWarpVecs) * 8) - 1));
 
   for (uint64_t t = t0; t < t1; t++) {
-    const uint64_t wv0 = vbeg + t * kSWarpVecs;
+    const uint64_t wv0 = vbeg + t * kSWarpVecs;  // first vector of this warp tile
     const uint64_t v0 = wv0 + lane;
+    const bool interior = wv0 * 8 >= s.lo && (wv0 + kSWarpVecs) * 8 <= s.hi;
+    uint4 v[kSV];
+    if (interior) {
+#pragma unroll
+      for (int k = 0; k < kSV; k++) v[k] = ld_stream(s.in + v0 + k * 32);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kSV; k++) {
+        const uint64_t vi = v0 + k * 32;
+        v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
+      }
+    }
+    uint32_t tail = 0;  // the unit after this warp tile (lane 31)
+    if (lane == 31) tail = unit_at(s, static_cast<int64_t>((wv0 + kSWarpVecs) * 8));
+    // String starts in [A0, A0 + 2048] (aligned coordinates; the last one is
+    // the unit after the tile).
     const int64_t A0 = static_cast<int64_t>(wv0 * 8) - phase;
     const int64_t A1 = A0 + kSWarpVecs * 8;
-    // Where the next tile's strings start: from the current window when it
-    // reaches (the common case), else by walking offsets.
-    const int rel = first_at_or_after(cur, A1);
-    uint64_t next_sidx;
-    if (rel >= 0) {
-      next_sidx = cur.base + rel;
-    } else {
-      next_sidx = cur.base + 64;
-      for (;;) {
-        const int64_t p = next_sidx + lane < count ? __ldg(offsets + next_sidx + lane) : INT64_MAX;
-        const uint32_t lt = __ballot_sync(kFull, p < A1);
-        next_sidx += __popc(lt);
-        if (lt != kFull) break;
-      }
-    }
-    // Prefetch the next tile (data + window) before repairing this one.
-    if (t + 1 < t1) {
-      load_data(nxt, t + 1);
-      load_window(nxt, next_sidx);
-    }
-    uint32_t tail = 0;
-    if (lane == 31) tail = unit_at(s, static_cast<int64_t>((wv0 + kSWarpVecs) * 8));
-
-    // String-start mask of this tile: entries of [cur.base, next_sidx] in [A0, A1].
     uint64_t M = 0;
     bool start_after = false;
-    {
-      auto mark = [&](int64_t p) {
-        uint32_t inr = __ballot_sync(kFull, p >= A0 && p < A1);
-        start_after |= __ballot_sync(kFull, p == A1) != 0;
-        while (inr) {
-          const int j = __ffs(inr) - 1;
-          inr &= inr - 1;
-          const uint32_t r = static_cast<uint32_t>(__shfl_sync(kFull, p, j) - A0);
-          if (lane == static_cast<int>((r >> 3) & 31)) M |= 1ull << (((r >> 8) << 3) | (r & 7));
-        }
-      };
-      mark(cur.w[0]);
-      mark(cur.w[1]);
-      // Windows beyond the first 64 entries (more than 64 starts in the tile).
-      for (uint64_t b = cur.base + 64; b <= next_sidx; b += 32) {
-        const int64_t p = b + lane < count ? __ldg(offsets + b + lane) : INT64_MAX;
-        mark(p);
+    uint64_t scan = sidx, next = sidx;
+    for (;;) {
+      const uint64_t idx = scan + lane;
+      const int64_t p = idx < count ? __ldg(offsets + idx) : INT64_MAX;
+      uint32_t inr = __ballot_sync(kFull, p >= A0 && p < A1);
+      start_after |= __ballot_sync(kFull, p == A1) != 0;
+      next += __popc(__ballot_sync(kFull, p < A1));
+      while (inr) {
+        const int j = __ffs(inr) - 1;
+        inr &= inr - 1;
+        const uint32_t r = static_cast<uint32_t>(__shfl_sync(kFull, p, j) - A0);  // unit within the tile
+        if (lane == static_cast<int>((r >> 3) & 31)) M |= 1ull << (((r >> 8) << 3) | (r & 7));
       }
+      if (__ballot_sync(kFull, p <= A1) != kFull) break;
+      scan += 32;
     }
-    const bool interior = wv0 * 8 >= s.lo && (wv0 + kSWarpVecs) * 8 <= s.hi;
+    sidx = next;
     if (!interior) {
 #pragma unroll
       for (int k = 0; k < kSV; k++) {
         const uint64_t vi = v0 + k * 32;
-        if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, cur.v[k]);
+        if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, v[k]);
       }
     }
+    // start flag of the unit after each vector: lane l+1's first unit of the
+    // same k, or lane 0's first unit of k+1 (lane 31); the tile's tail for k=7.
     uint32_t F = 0;
 #pragma unroll
     for (int k = 0; k < kSV; k++) F |= static_cast<uint32_t>((M >> (8 * k)) & 1u) << k;
     const uint32_t Fd = __shfl_sync(kFull, F, (lane + 1) & 31);
     const uint32_t after = lane == 31 ? ((Fd >> 1) | (start_after ? (1u << (kSV - 1)) : 0u)) : Fd;
 
-    Flags f = classify8(cur.v[0]);
+    Flags cur = classify8(v[0]);
     const uint32_t tail_l = lflag_lo(tail);
 #pragma unroll
     for (int k = 0; k < kSV; k++) {
-      Flags fn;
-      if (k + 1 < kSV) fn = classify8(cur.v[k + 1]);
-      const uint32_t up = __shfl_sync(kFull, f.H1, (lane + 31) & 31);
-      const uint32_t dn = __shfl_sync(kFull, f.L0, (lane + 1) & 31);
+      Flags nxt;
+      if (k + 1 < kSV) nxt = classify8(v[k + 1]);
+      const uint32_t up = __shfl_sync(kFull, cur.H1, (lane + 31) & 31);
+      const uint32_t dn = __shfl_sync(kFull, cur.L0, (lane + 1) & 31);
       uint32_t ln = dn;
       if (k + 1 < kSV) {
-        const uint32_t dn_next = __shfl_sync(kFull, fn.L0, (lane + 1) & 31);
+        const uint32_t dn_next = __shfl_sync(kFull, nxt.L0, (lane + 1) & 31);
         if (lane == 31) ln = dn_next;
       } else if (lane == 31) {
         ln = tail_l;
@@ -317,25 +276,24 @@ __global__ void __launch_bounds__(kSThreads, 2) batched_stream_kernel(Span s, co
       hp_carry = up;
       const uint32_t bits = static_cast<uint32_t>(M >> (8 * k)) & 0xFFu;
       uint32_t B0, B1;
-      bad8(f, hp, ln, B0, B1, spread4(bits), spread4(bits >> 4), ((after >> k) & 1u) << 7);
+      bad8(cur, hp, ln, B0, B1, spread4(bits), spread4(bits >> 4), ((after >> k) & 1u) << 7);
       const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
       const uint64_t vi = v0 + k * 32;
       if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
-        if (store) st_stream(s.out + vi, blend(cur.v[k], B0, B1));
+        if (store) st_stream(s.out + vi, blend(v[k], B0, B1));
       } else if (store && vi < vend) {
-        const uint4 r = blend(cur.v[k], B0, B1);
+        const uint4 r = blend(v[k], B0, B1);
 #pragma unroll
         for (int j = 0; j < 8; j++) {
           const uint64_t a = vi * 8 + j;
           if (a >= s.lo && a < s.hi) {
             const uint32_t u = get_unit(r, j);
-            if (!kInPlace || u != get_unit(cur.v[k], j)) s.out_units[a - s.lo] = static_cast<uint16_t>(u);
+            if (!kInPlace || u != get_unit(v[k], j)) s.out_units[a - s.lo] = static_cast<uint16_t>(u);
           }
         }
       }
-      if (k + 1 < kSV) f = fn;
+      if (k + 1 < kSV) cur = nxt;
     }
-    cur = nxt;
   }
 }
 
@@ -355,7 +313,7 @@ cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, si
   s.prefetch_tiles = 0;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = static_cast<unsigned>(sms * 2);
+  const unsigned grid = static_cast<unsigned>(sms * 3);
   const uint64_t count = static_cast<uint64_t>(num_strings) + 1;
   if (in != out) {
     batched_stream_kernel<false, 1><<<grid, kSThreads, 0, stream>>>(s, offsets, count, ph);
