@@ -34,7 +34,8 @@ namespace tma {
 
 constexpr int kConsumerWarps = kWarps;             // 8 warps x 32 lanes x kVecs vectors
 constexpr int kThreadsTma = (kConsumerWarps + 1) * 32;
-constexpr int kStages = 6;
+constexpr int kStages = 4;
+constexpr int kTmaCtasPerSm = 3;
 constexpr int kTileBytes = kCtaVecs * 16;          // 16 KiB
 constexpr int kBitmapWords = kCtaUnits / 32 + 2;   // string starts of one tile (+1 unit)
 constexpr int kStageBytes = 16 + kTileBytes + 16 + kBitmapWords * 4 + 8;  // pre | tile | post | bitmap
@@ -137,7 +138,7 @@ __device__ __forceinline__ uint64_t lower_bound32(const int64_t* off, uint64_t c
 }
 
 template <int kInPlace, bool kBatched, int kGran>
-__global__ void __launch_bounds__(kThreadsTma, 2) repair_tma_kernel(Span s, BatchArgsT b) {
+__global__ void __launch_bounds__(kThreadsTma, kTmaCtasPerSm) repair_tma_kernel(Span s, BatchArgsT b) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageStride);
@@ -334,7 +335,7 @@ cudaError_t launch_tma(const Span& s, const BatchArgsT& b, uint64_t ntiles_hint,
       g_attr_set[idx][dev][kGran] = true;
     }
   }
-  uint64_t grid = static_cast<uint64_t>(dev < 64 ? g_sms[dev] : 148) * 2;
+  uint64_t grid = static_cast<uint64_t>(dev < 64 ? g_sms[dev] : 148) * kTmaCtasPerSm;
   if (ntiles_hint > 0 && ntiles_hint < grid) grid = ntiles_hint;
   repair_tma_kernel<kInPlace, kBatched, kGran><<<static_cast<unsigned>(grid), kThreadsTma, kSmemBytes, stream>>>(s, b);
   note_launch();
