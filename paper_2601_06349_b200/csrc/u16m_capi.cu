@@ -134,6 +134,28 @@ HostPipe* pipe_for(int device, u16m_status* st) {
   return p;
 }
 
+// Host-path mode (U16M_HOST_MODE: "auto" = zero-copy for pinned mapped
+// buffers else staged; "staged" forces the copy pipeline). 0 auto, 1 staged.
+int host_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("U16M_HOST_MODE");
+    return (e && std::strcmp(e, "staged") == 0) ? 1 : 0;
+  }();
+  return m;
+}
+
+// Device address of a pinned host buffer mapped into the device's address
+// space (cudaHostAlloc / cudaHostRegister memory under UVA), else nullptr.
+const uint16_t* mapped_device_ptr(const uint16_t* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return nullptr;
+  return static_cast<const uint16_t*>(a.devicePointer);
+}
+
 // ---- shard driver state ------------------------------------------------------
 std::mutex g_peer_mu;
 std::vector<std::pair<int, int>> g_peer_enabled;
@@ -310,6 +332,26 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
   HostPipe* p = pipe_for(dev, &st);
   if (p == nullptr) return st;
   const bool be = byte_order == U16M_BIG_ENDIAN;
+  // Zero-copy path: pinned, device-mapped host buffers are repaired by the
+  // stream kernel straight over PCIe — no staging copies. In place this moves
+  // every input byte host->device once but only the 32-byte sectors that hold
+  // a rewrite device->host, so it beats the staged pipeline's full D2H.
+  const uint16_t* din = mapped_device_ptr(in);
+  uint16_t* dout = const_cast<uint16_t*>(mapped_device_ptr(out));
+  if (din && dout && host_mode() != 1) {
+    if (replacements) {
+      e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
+      if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+    }
+    e = byte_order < 0 ? u16m::launch_repair(din, n, dout, -1, -1, nullptr, nullptr, p->comp)
+                       : u16m::launch_fix_bytes(din, n, dout, be, replacements ? p->counter : nullptr, p->comp, -1, -1);
+    if (e != cudaSuccess) return cuda_fail(e, "zero-copy repair kernel launch");
+    e = cudaStreamSynchronize(p->comp);
+    if (e == cudaSuccess && replacements)
+      e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "zero-copy repair");
+    return U16M_OK;
+  }
   auto unit = [&](size_t i) -> int32_t {  // unit value of in[i] in the job's byte order
     const uint32_t w = in[i];
     return static_cast<int32_t>(be ? (((w & 0xFFu) << 8) | (w >> 8)) : w);
