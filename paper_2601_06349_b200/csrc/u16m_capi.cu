@@ -134,12 +134,19 @@ HostPipe* pipe_for(int device, u16m_status* st) {
   return p;
 }
 
-// Host-path mode (U16M_HOST_MODE: "auto" = zero-copy for pinned mapped
-// buffers else staged; "staged" forces the copy pipeline). 0 auto, 1 staged.
+// Host-path mode (U16M_HOST_MODE), for A/B runs:
+//   auto (0): in-place jobs on pinned mapped buffers stage H2D by copy engine
+//             and write back only rewritten 32-byte groups straight into host
+//             memory from the kernel (no D2H copy); everything else staged.
+//   staged (1): H2D copy -> kernel -> D2H copy for every job.
+//   zerocopy (2): the kernel reads and writes the mapped host buffers directly.
+enum HostMode { kHostAuto = 0, kHostStaged = 1, kHostZeroCopy = 2 };
 int host_mode() {
   static const int m = [] {
     const char* e = std::getenv("U16M_HOST_MODE");
-    return (e && std::strcmp(e, "staged") == 0) ? 1 : 0;
+    if (e && std::strcmp(e, "staged") == 0) return int(kHostStaged);
+    if (e && std::strcmp(e, "zerocopy") == 0) return int(kHostZeroCopy);
+    return int(kHostAuto);
   }();
   return m;
 }
@@ -332,13 +339,11 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
   HostPipe* p = pipe_for(dev, &st);
   if (p == nullptr) return st;
   const bool be = byte_order == U16M_BIG_ENDIAN;
-  // Zero-copy path: pinned, device-mapped host buffers are repaired by the
-  // stream kernel straight over PCIe — no staging copies. In place this moves
-  // every input byte host->device once but only the 32-byte sectors that hold
-  // a rewrite device->host, so it beats the staged pipeline's full D2H.
+  // Zero-copy (A/B): the stream kernel reads and writes the mapped host
+  // buffers directly over PCIe — no staging copies.
   const uint16_t* din = mapped_device_ptr(in);
   uint16_t* dout = const_cast<uint16_t*>(mapped_device_ptr(out));
-  if (din && dout && host_mode() != 1) {
+  if (din && dout && host_mode() == kHostZeroCopy) {
     if (replacements) {
       e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
       if (e != cudaSuccess) return cuda_fail(e, "counter reset");
@@ -360,31 +365,42 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
     e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
   }
+  // Write-back mode (default for in-place jobs on pinned mapped memory): the
+  // host buffer already holds the input, so instead of a D2H copy of every
+  // chunk the kernel stores only the 32-byte groups that hold a rewrite
+  // straight into host memory. H2D (copy engine) and those posted writes use
+  // opposite PCIe directions.
+  const bool writeback = in == out && dout != nullptr && host_mode() == kHostAuto &&
+                         ((reinterpret_cast<uintptr_t>(dout) ^ reinterpret_cast<uintptr_t>(p->dbuf[0])) & 15u) == 0;
   size_t c = 0;
   const size_t chunk = pipe_chunk_units();
   for (size_t c0 = 0; c0 < n; c0 += chunk, c++) {
     const size_t len = std::min(chunk, n - c0);
     const int k = static_cast<int>(c % kRing);
     // Halo units are read from the host copy at enqueue time. For in-place
-    // jobs an earlier chunk's D2H may already have rewritten in[c0-1]; that
-    // is benign (a unit is only rewritten when no neighbour pairs with it).
+    // jobs an earlier chunk's write-back may already have rewritten in[c0-1];
+    // that is benign (a unit is only rewritten when no neighbour pairs with it).
     const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
     const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
     if (c >= static_cast<size_t>(kRing)) {
-      e = cudaStreamWaitEvent(p->h2d, p->drained[k], 0);
+      e = cudaStreamWaitEvent(p->h2d, writeback ? p->repaired[k] : p->drained[k], 0);
       if (e != cudaSuccess) return cuda_fail(e, "pipeline wait");
     }
     e = cudaMemcpyAsync(p->dbuf[k], in + c0, len * 2, cudaMemcpyHostToDevice, p->h2d);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
     cudaEventRecord(p->loaded[k], p->h2d);
     cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-    if (byte_order < 0)
+    if (writeback)
+      e = u16m::launch_stream_writeback(p->dbuf[k], len, dout + c0, left, right, be,
+                                        replacements ? p->counter : nullptr, p->comp);
+    else if (byte_order < 0)
       e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, p->comp);
     else
       e = u16m::launch_fix_bytes(p->dbuf[k], len, p->dbuf[k], be, replacements ? p->counter : nullptr, p->comp,
                                  left, right);
     if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
     cudaEventRecord(p->repaired[k], p->comp);
+    if (writeback) continue;
     cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
     e = cudaMemcpyAsync(out + c0, p->dbuf[k], len * 2, cudaMemcpyDeviceToHost, p->d2h);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy");

@@ -406,6 +406,35 @@ cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long lo
   return cudaGetLastError();
 }
 
+cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
+                                   bool big_endian, unsigned long long* count, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
+  if ((ia ^ oa) & 15u) return cudaErrorInvalidValue;
+  const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
+  Span s;
+  s.in = reinterpret_cast<const uint4*>(ia - 2 * ph);
+  s.out = reinterpret_cast<uint4*>(oa - 2 * ph);
+  s.out_units = out;
+  s.lo = ph;
+  s.hi = ph + n;
+  s.left = left;
+  s.right = right;
+  s.left_ptr = s.right_ptr = nullptr;
+  s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
+  constexpr int kCtaVecs = (kSThreads / 32) * 32 * 8;
+  const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kCtaVecs - 1) / kCtaVecs;
+  const unsigned g = static_cast<unsigned>(ntiles);
+  // The in-place instantiation writes only 32-byte groups holding a rewrite,
+  // here into a different buffer that already holds the input.
+  if (big_endian) launch_codec_t<true, true>(s, g, count, stream);
+  else launch_codec_t<true, false>(s, g, count, stream);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream) {
   switch (stream_vecs()) {
     case 12: return launch_stream_v<12, 3>(s, part, stream);
