@@ -134,19 +134,22 @@ HostPipe* pipe_for(int device, u16m_status* st) {
   return p;
 }
 
-// Host-path mode (U16M_HOST_MODE), for A/B runs:
-//   auto (0): in-place jobs on pinned mapped buffers stage H2D by copy engine
-//             and write back only rewritten 32-byte groups straight into host
-//             memory from the kernel (no D2H copy); everything else staged.
-//   staged (1): H2D copy -> kernel -> D2H copy for every job.
-//   zerocopy (2): the kernel reads and writes the mapped host buffers directly.
-enum HostMode { kHostAuto = 0, kHostStaged = 1, kHostZeroCopy = 2 };
+// Host-path mode (U16M_HOST_MODE). Measured on the B200 box (scripts/
+// e2e_probe.py, 512 MiB, input GB/s, in place / copy):
+//   staged (default): H2D copy -> kernel -> D2H copy, 3 streams   39.6-41.9 / 42-46
+//   writeback: in-place jobs on pinned mapped memory stage H2D by copy engine
+//              and the kernel stores only rewritten 32-byte groups straight
+//              into host memory (no D2H copy)                          36.0 / —
+//   zerocopy: the kernel reads and writes mapped host buffers directly  36.4 / 38.5
+// Small posted PCIe writes from SMs cost more than a full-duplex DMA copy, so
+// the copy-engine pipeline stays the default.
+enum HostMode { kHostStaged = 0, kHostWriteback = 1, kHostZeroCopy = 2 };
 int host_mode() {
   static const int m = [] {
     const char* e = std::getenv("U16M_HOST_MODE");
-    if (e && std::strcmp(e, "staged") == 0) return int(kHostStaged);
+    if (e && std::strcmp(e, "writeback") == 0) return int(kHostWriteback);
     if (e && std::strcmp(e, "zerocopy") == 0) return int(kHostZeroCopy);
-    return int(kHostAuto);
+    return int(kHostStaged);
   }();
   return m;
 }
@@ -365,12 +368,10 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
     e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
   }
-  // Write-back mode (default for in-place jobs on pinned mapped memory): the
-  // host buffer already holds the input, so instead of a D2H copy of every
-  // chunk the kernel stores only the 32-byte groups that hold a rewrite
-  // straight into host memory. H2D (copy engine) and those posted writes use
-  // opposite PCIe directions.
-  const bool writeback = in == out && dout != nullptr && host_mode() == kHostAuto &&
+  // Write-back mode (A/B): the host buffer already holds the input, so
+  // instead of a D2H copy of every chunk the kernel stores only the 32-byte
+  // groups that hold a rewrite straight into host memory.
+  const bool writeback = in == out && dout != nullptr && host_mode() == kHostWriteback &&
                          ((reinterpret_cast<uintptr_t>(dout) ^ reinterpret_cast<uintptr_t>(p->dbuf[0])) & 15u) == 0;
   size_t c = 0;
   const size_t chunk = pipe_chunk_units();

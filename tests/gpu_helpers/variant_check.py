@@ -58,6 +58,17 @@ def main():
     t = dev(data)
     P.to_well_formed_batched(t, torch.from_numpy(offs).cuda(), out=t)
     assert (host(t) == e).all(), "batched in place"
+    # host-memory path (staged / writeback / zerocopy per U16M_HOST_MODE), pinned buffers
+    y = O.gen_config(1, 300_001, seed=8)
+    pin = torch.from_numpy(y.view(np.int16).copy()).pin_memory()
+    outp = torch.empty_like(pin).pin_memory()
+    L = P._lib.raw()
+    assert L.u16m_to_well_formed_host(pin.data_ptr(), y.size, outp.data_ptr()) == 0
+    assert (outp.numpy().view(np.uint16) == O.stencil(y)).all(), "host copy"
+    assert L.u16m_to_well_formed_host(pin.data_ptr(), y.size, pin.data_ptr()) == 0
+    assert (pin.numpy().view(np.uint16) == O.stencil(y)).all(), "host in place"
+    be, c = P.fix_utf16_bytes(y.astype(">u2").tobytes(), "be")
+    assert np.frombuffer(be, ">u2").astype(np.uint16).tobytes() == O.stencil(y).tobytes(), "host codec"
     torch.cuda.synchronize()
     print("OK", {k: v for k, v in os.environ.items() if k.startswith("U16M_")})
 
