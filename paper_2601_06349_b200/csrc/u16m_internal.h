@@ -50,8 +50,6 @@ cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out,
 // Batched form on persistent warps with the rolling register pipeline.
 cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
                                   cudaStream_t stream);
-// Warp-pipelined cp.async kernel (u16m_pipe.cu): whole same-phase jobs.
-cudaError_t launch_pipe(const Span& s, cudaStream_t stream);
 
 // §8(f-3): byte-order-aware repair + replacement count (same 16-byte phase).
 // left/right: halo UNIT values (byte order already resolved), -1 = outside.

@@ -400,9 +400,10 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 // copy, config 1 in 133 us), the batched form runs the TMA-pipelined kernel
 // (its producer warp walks the offsets off the consumers' critical path).
 // U16M_KERNEL overrides for A/B runs (profiles/README.md has the numbers):
-// "tma" (TMA-pipelined for everything), "pipe" (per-warp cp.async rings for
-// whole copy / in-place jobs), "general" (the 4-vector general kernel).
-enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoicePipe = 3 };
+// "tma" (TMA-pipelined for everything), "ldg" (register-staged everywhere,
+// including the batched form on persistent warps), "general" (the 4-vector
+// general kernel).
+enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoiceLdg = 3 };
 // (kChoiceGeneral and kChoiceAuto share the register-staged kernel for plain
 // streams; they differ for the batched form.)
 static int kernel_choice() {
@@ -410,7 +411,7 @@ static int kernel_choice() {
     const char* e = std::getenv("U16M_KERNEL");
     if (e && std::strcmp(e, "tma") == 0) return int(kChoiceTma);
     if (e && std::strcmp(e, "general") == 0) return int(kChoiceGeneral);
-    if (e && std::strcmp(e, "pipe") == 0) return int(kChoicePipe);
+    if (e && std::strcmp(e, "ldg") == 0) return int(kChoiceLdg);
     return int(kChoiceAuto);
   }();
   return choice;
@@ -444,9 +445,7 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
     if (part == kTilesInterior) return cudaSuccess;
     return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
   }
-  if ((in == out || same) && choice == kChoicePipe && part == kTilesAll) return launch_pipe(s, stream);
-  if ((in == out || same) && (choice == kChoiceAuto || choice == kChoicePipe))
-    return launch_stream(s, part, stream);
+  if ((in == out || same) && (choice == kChoiceAuto || choice == kChoiceLdg)) return launch_stream(s, part, stream);
   s.tile_sel = part;
   const uint64_t grid = part == kTilesAll ? ntiles
                         : part == kTilesEdges ? (ntiles < 2 ? ntiles : 2)
@@ -557,7 +556,7 @@ cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t nu
   const bool same16 = ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
   if ((kernel_choice() == kChoiceTma || kernel_choice() == kChoiceAuto) && same16)
     return launch_batched_tma(in, offsets, num_strings, out, stream);
-  if (kernel_choice() == kChoicePipe && same16) return launch_batched_stream(in, offsets, num_strings, out, stream);
+  if (kernel_choice() == kChoiceLdg && same16) return launch_batched_stream(in, offsets, num_strings, out, stream);
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
   const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
