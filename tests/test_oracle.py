@@ -189,3 +189,33 @@ def test_oracle_vs_reference_build():
         b = np.empty_like(a)
         O.ref().ref_generate(10_000, 0.05, 0.05, seed, O._p16(b))
         assert (a == b).all()
+
+
+def test_in_place_race_is_benign_exhaustively():
+    """SURVEY.md §0 fact 3, checked over every 5-unit class window: when a
+    neighbour reads a unit either before or after that unit's own in-place
+    rewrite (in any combination), every decision is unchanged. Classes:
+    N (non-surrogate), H, L; edges are N."""
+    import itertools
+
+    vals = {"N": 0x41, "H": 0xD800, "L": 0xDC00}
+    for w in itertools.product("NHL", repeat=5):
+        x = np.array([vals[c] for c in w], np.uint16)
+        truth = O.stencil(x)
+        # every subset of units already rewritten when the neighbours look
+        for mask in range(32):
+            seen = x.copy()
+            for i in range(5):
+                if mask >> i & 1:
+                    seen[i] = truth[i]
+            # decisions of the three interior units from the mixed view
+            for i in (1, 2, 3):
+                u = int(x[i])
+                prev_h = (int(seen[i - 1]) & 0xFC00) == 0xD800
+                next_l = (int(seen[i + 1]) & 0xFC00) == 0xDC00
+                r = u
+                if (u & 0xFC00) == 0xD800 and not next_l:
+                    r = 0xFFFD
+                if (u & 0xFC00) == 0xDC00 and not prev_h:
+                    r = 0xFFFD
+                assert r == truth[i], (w, mask, i)
