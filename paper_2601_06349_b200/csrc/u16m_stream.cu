@@ -33,7 +33,8 @@ constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;  // 2048 vectors = 32 K
 // kBE: units are big-endian in memory (fused byte-order handling, §8(f-3));
 // kCount: add the number of rewritten units to *count (warp reduction, one
 // atomic per warp).
-template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false>
+template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false,
+          int kHint = 0>
 __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count) {
   constexpr int kSWarpVecs = 32 * kSV;
   constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   if (interior) {
     const uint4* src = s.in + v0;
 #pragma unroll
-    for (int k = 0; k < kSV; k++) v[k] = ld_stream(src + k * 32);
+    for (int k = 0; k < kSV; k++) v[k] = ld_hint<kHint / 4>(src + k * 32);
     const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
     if (lane == 0) halo = to_mem<kBE>(src16[-1]);
     if (lane == 31) halo = to_mem<kBE>(src16[(kSV - 1) * 32 * 8 + 8]);
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
 #pragma unroll
     for (int k = 0; k < kSV; k++) {
       const uint64_t vi = v0 + k * 32;
-      v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
+      v[k] = vi < vend ? ld_hint<kHint / 4>(s.in + vi) : make_uint4(0, 0, 0, 0);
     }
     // unit_at returns unit values for halos but raw memory words in range.
     const uint64_t warp_v0 = v0 - lane;
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
       if (vi < vend) counted += __popc(c0) + __popc(c1);
     }
     if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
-      if (store) st_stream(dst + k * 32, blend<kBE>(v[k], B0, B1));
+      if (store) st_hint<kHint % 4>(dst + k * 32, blend<kBE>(v[k], B0, B1));
     } else if (store && vi < vend) {
       const uint4 r = blend<kBE>(v[k], B0, B1);
 #pragma unroll
@@ -347,6 +348,22 @@ static int prefetch_setting() {
   return v;
 }
 
+static int hint_setting() {
+  static const int v = [] {
+    const char* l = std::getenv("U16M_LDHINT");
+    const char* t = std::getenv("U16M_STHINT");
+    const int ld = l ? std::atoi(l) : 0, st = t ? std::atoi(t) : 0;
+    return (ld >= 0 && ld < 4 ? ld : 0) * 4 + (st == 1 ? 1 : 0);
+  }();
+  return v;
+}
+
+template <int kHint>
+static void launch_hinted(const Span& s, unsigned g, cudaStream_t stream) {
+  if (s.in != s.out) stream_kernel<false, 1, 8, 4, false, false, kHint><<<g, kSThreads, 0, stream>>>(s, nullptr);
+  else stream_kernel<true, 2, 8, 4, false, false, kHint><<<g, kSThreads, 0, stream>>>(s, nullptr);
+}
+
 template <int kV, int kMB>
 static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
   constexpr int kCtaVecs = (kSThreads / 32) * 32 * kV;
@@ -366,6 +383,20 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
     s.prefetch_tiles = pf >= 0 ? pf : (ntiles > static_cast<uint64_t>(2 * sms * kMB) ? sms * kMB : 0);
   }
   const unsigned g = static_cast<unsigned>(grid);
+  const int hint = hint_setting();
+  if (kV == 8 && hint != 0 && (s.in != s.out || inplace_granularity() == 2)) {
+    switch (hint) {
+      case 1: launch_hinted<1>(s, g, stream); break;
+      case 4: launch_hinted<4>(s, g, stream); break;
+      case 5: launch_hinted<5>(s, g, stream); break;
+      case 8: launch_hinted<8>(s, g, stream); break;
+      case 9: launch_hinted<9>(s, g, stream); break;
+      case 12: launch_hinted<12>(s, g, stream); break;
+      default: launch_hinted<13>(s, g, stream); break;
+    }
+    note_launch();
+    return cudaGetLastError();
+  }
   if (s.in != s.out) {
     stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr);
   } else {
