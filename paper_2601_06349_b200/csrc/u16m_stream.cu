@@ -43,9 +43,15 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   const uint64_t vbeg = s.lo / 8;
   const uint64_t vend = (s.hi + 7) / 8;
   const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
-  uint64_t tile = blockIdx.x;
-  if (s.tile_sel == kTilesEdges) tile = blockIdx.x == 0 ? 0 : ntiles - 1;
-  if (s.tile_sel == kTilesInterior) tile = blockIdx.x + 1;
+  uint64_t nwork = ntiles;
+  if (s.tile_sel == kTilesEdges) nwork = ntiles < 2 ? ntiles : 2;
+  if (s.tile_sel == kTilesInterior) nwork = ntiles > 2 ? ntiles - 2 : 0;
+  uint32_t counted = 0;
+  // One tile per CTA normally; a smaller (persistent) grid strides over tiles.
+  for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+  uint64_t tile = w;
+  if (s.tile_sel == kTilesEdges) tile = w == 0 ? 0 : ntiles - 1;
+  if (s.tile_sel == kTilesInterior) tile = w + 1;
   const uint64_t tv0 = vbeg + tile * kSCtaVecs;
   const bool interior = tv0 * 8 > s.lo && (tv0 + kSCtaVecs) * 8 < s.hi;
   const uint64_t v0 = tv0 + lane_off;  // this lane's vector k sits at v0 + 32k
@@ -90,7 +96,6 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
       if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges<kBE>(s, vi, v[k]);
     }
   }
-  uint32_t counted = 0;
 
   // Rolling pipeline over k: flags of vector k (cur) and k+1 (nxt) live.
   Flags cur = classify8<kBE>(v[0]);
@@ -136,6 +141,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
     }
     if (k + 1 < kSV) cur = nxt;
   }
+  }  // tile loop
   if constexpr (kCount) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) counted += __shfl_xor_sync(kFull, counted, o);
@@ -348,6 +354,14 @@ static int prefetch_setting() {
   return v;
 }
 
+static int persist_setting() {  // U16M_PERSIST=N: grid of N CTAs per SM (A/B)
+  static const int v = [] {
+    const char* e = std::getenv("U16M_PERSIST");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 static int hint_setting() {
   static const int v = [] {
     const char* l = std::getenv("U16M_LDHINT");
@@ -381,6 +395,13 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
     // auto: one resident wave ahead, and only for jobs of more than two waves
     // (measured: +3% on config 1, a small loss on the 2-wave config 0).
     s.prefetch_tiles = pf >= 0 ? pf : (ntiles > static_cast<uint64_t>(2 * sms * kMB) ? sms * kMB : 0);
+  }
+  if (persist_setting() > 0) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t cap = static_cast<uint64_t>(sms) * persist_setting();
+    if (grid > cap) grid = cap;
+    s.prefetch_tiles = 0;
   }
   const unsigned g = static_cast<unsigned>(grid);
   const int hint = hint_setting();
