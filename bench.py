@@ -301,8 +301,8 @@ def run_ours(args):
 
     def step_kernel():
         if mode == "batched":
-            _lib._check(L.u16m_to_well_formed_batched(data.data_ptr(), offsets.data_ptr(), offsets.numel() - 1,
-                                                     out.data_ptr(), sptr))
+            _lib._check(L.u16m_to_well_formed_batched_n(data.data_ptr(), data.numel(), offsets.data_ptr(),
+                                                       offsets.numel() - 1, out.data_ptr(), sptr))
         elif distributed:
             pdist.repair_shard(data, out)
         elif mode == "inplace":

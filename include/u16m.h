@@ -61,6 +61,15 @@ u16m_status u16m_to_well_formed_in_place(uint16_t* buf, size_t n, void* stream);
 u16m_status u16m_to_well_formed_batched(const uint16_t* in, const int64_t* offsets,
                                         size_t num_strings, uint16_t* out, void* stream);
 
+/* Same, with the length of the in/out buffers (units) known to the caller —
+ * the form the C++, Python and CLI front ends use. The grid is sized from
+ * n_units (no host sync), strings are located through a per-tile table built
+ * by a pre-pass, and every CTA streams one tile (the fastest form measured).
+ * Requires offsets[num_strings] <= n_units (units past n_units are never
+ * touched). Allocates a small stream-ordered workspace (cudaMallocAsync). */
+u16m_status u16m_to_well_formed_batched_n(const uint16_t* in, size_t n_units, const int64_t* offsets,
+                                          size_t num_strings, uint16_t* out, void* stream);
+
 /* One contiguous piece of a larger logical buffer (the per-shard primitive for
  * one-process-per-GPU callers). `left`/`right` are the units just outside
  * [0,n) in the logical buffer, or -1 where the logical buffer ends. Device

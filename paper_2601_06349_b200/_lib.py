@@ -32,6 +32,7 @@ _st = ctypes.c_int
 _L.u16m_to_well_formed.argtypes = [_u16p, _sz, _u16p, _vp]
 _L.u16m_to_well_formed_in_place.argtypes = [_u16p, _sz, _vp]
 _L.u16m_to_well_formed_batched.argtypes = [_u16p, _vp, _sz, _u16p, _vp]
+_L.u16m_to_well_formed_batched_n.argtypes = [_u16p, _sz, _vp, _sz, _u16p, _vp]
 _L.u16m_to_well_formed_halo.argtypes = [_u16p, _sz, _u16p, ctypes.c_int32, ctypes.c_int32, _vp]
 _L.u16m_to_well_formed_halo_ptr.argtypes = [_u16p, _sz, _u16p, _vp, _vp, _vp]
 _L.u16m_to_well_formed_part.argtypes = [_u16p, _sz, _u16p, _vp, _vp, ctypes.c_int, _vp]
@@ -54,6 +55,7 @@ _L.u16m_fix_utf16_bytes.argtypes = [_vp, _sz, _vp, ctypes.c_int, _vp, _vp]
 _L.u16m_fix_utf16_bytes_host.argtypes = [_vp, _sz, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong)]
 _L.u16m_unpaired_offsets_host.argtypes = [_vp, _sz, _sz, _vp, ctypes.POINTER(ctypes.c_size_t)]
 for _f in ("u16m_to_well_formed", "u16m_to_well_formed_in_place", "u16m_to_well_formed_batched",
+           "u16m_to_well_formed_batched_n",
            "u16m_to_well_formed_halo", "u16m_to_well_formed_halo_ptr", "u16m_to_well_formed_sharded",
            "u16m_to_well_formed_host", "u16m_to_well_formed_part", "u16m_count_unpaired", "u16m_unpaired_offsets",
            "u16m_gen_config", "u16m_gen_c3_offsets", "u16m_gen_c3_content",
@@ -178,9 +180,11 @@ def to_well_formed_batched(data: torch.Tensor, offsets: torch.Tensor, out: Optio
     if out is None:
         out = data.clone()
     _units(out, "out")
+    if out.numel() != data.numel():
+        raise ValueError("to_well_formed_batched: input and output lengths differ")
     with torch.cuda.device(data.device):
-        _check(_L.u16m_to_well_formed_batched(data.data_ptr(), offsets.data_ptr(), offsets.numel() - 1,
-                                              out.data_ptr(), _stream(data, stream)))
+        _check(_L.u16m_to_well_formed_batched_n(data.data_ptr(), data.numel(), offsets.data_ptr(),
+                                                offsets.numel() - 1, out.data_ptr(), _stream(data, stream)))
     return out
 
 

@@ -297,6 +297,23 @@ u16m_status u16m_fix_utf16_bytes(const void* in, size_t n_units, void* out, int 
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "codec repair kernel launch");
 }
 
+u16m_status u16m_to_well_formed_batched_n(const uint16_t* in, size_t n_units, const int64_t* offsets,
+                                          size_t num_strings, uint16_t* out, void* stream) {
+  if (offsets == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "offsets is null");
+  if (num_strings == 0 || n_units == 0) return U16M_OK;
+  U16M_TRY(check_pair(in, n_units, out));
+  if (reinterpret_cast<uintptr_t>(offsets) & 7u) return fail(U16M_ERR_MISALIGNED, "offsets must be 8-byte aligned");
+  U16M_TRY(check_device_present());
+  U16M_TRY(check_device_ptr(in, "in"));
+  if (out != in) U16M_TRY(check_device_ptr(out, "out"));
+  U16M_TRY(check_device_ptr(offsets, "offsets"));
+  const bool same16 = ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
+  const cudaError_t e = same16 && u16m::batched_tiles_enabled()
+                            ? u16m::launch_batched_tiles(in, n_units, offsets, num_strings, out, as_stream(stream))
+                            : u16m::launch_batched(in, offsets, num_strings, out, as_stream(stream));
+  return e == cudaSuccess ? U16M_OK : cuda_fail(e, "batched repair kernel launch");
+}
+
 u16m_status u16m_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
                                 void* stream) {
   if (count_out == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "count_out is null");

@@ -551,6 +551,13 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   return e != cudaSuccess ? e : f;
 }
 
+// The length-aware batched form runs the tile kernel unless an A/B choice
+// pins another family ("tma" / "general").
+bool batched_tiles_enabled() {
+  const int c = kernel_choice();
+  return c == kChoiceAuto || c == kChoiceLdg;
+}
+
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream) {
   const bool same16 = ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0;

@@ -304,6 +304,184 @@ __global__ void __launch_bounds__(kSThreads, 3) batched_stream_kernel(Span s, co
   }
 }
 
+// ---- batched form, non-persistent (buffer length known) ----------------------
+// Persistent grids measured 15-20 % slower than one-tile-per-CTA grids for
+// register-staged streaming (U16M_PERSIST), so the batched form also runs one
+// 16384-unit tile per CTA. The grid is sized from the caller's buffer length
+// (tiles past offsets[S] exit); a pre-pass scatters, per string, its index
+// into the table of "first string starting in or after tile t", so a CTA
+// finds its strings with two dependent loads (table, then a 32-entry window
+// of offsets per warp) issued after — and overlapping — its 8 data loads.
+__global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t count, uint32_t phase,
+                                  uint64_t* __restrict__ tile_first, uint64_t ntiles_max) {
+  const uint64_t s_idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (s_idx >= count) return;
+  const int64_t A = __ldg(offsets);
+  const int64_t base = ((A + phase) / 8) * 8 - phase;  // key of tile 0
+  constexpr int64_t kTileUnits = kSThreads / 32 * kSWarpVecs * 8;
+  const int64_t p = __ldg(offsets + s_idx);
+  uint64_t t_hi = static_cast<uint64_t>((p - base) / kTileUnits);
+  uint64_t t_lo = s_idx ? static_cast<uint64_t>((__ldg(offsets + s_idx - 1) - base) / kTileUnits) + 1 : 0;
+  if (t_hi >= ntiles_max) t_hi = ntiles_max - 1;
+  for (uint64_t t = t_lo; t <= t_hi; t++) tile_first[t] = s_idx;
+}
+
+template <bool kInPlace, int kGran>
+__global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, const int64_t* __restrict__ offsets,
+                                                                    uint64_t count, uint32_t phase,
+                                                                    const uint64_t* __restrict__ tile_first,
+                                                                    int64_t n_units) {
+  const int lane = threadIdx.x & 31;
+  {
+    // Clamp to the caller's buffer: offsets beyond it are a contract error,
+    // and must not turn into out-of-bounds accesses.
+    int64_t A = __ldg(offsets), B = __ldg(offsets + count - 1);
+    B = B < n_units ? B : n_units;
+    A = A < B ? A : B;
+    s.lo = static_cast<uint64_t>(A) + phase;
+    s.hi = static_cast<uint64_t>(B) + phase;
+    s.out_units = reinterpret_cast<uint16_t*>(s.out) + s.lo;
+  }
+  if (s.hi <= s.lo) return;
+  const uint64_t vbeg = s.lo / 8;
+  const uint64_t vend = (s.hi + 7) / 8;
+  const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
+  const uint64_t tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  const uint64_t tv0 = vbeg + tile * kSCtaVecs;
+  const uint64_t wv0 = tv0 + threadIdx.x / 32 * kSWarpVecs;
+  const uint64_t v0 = wv0 + lane;
+  const bool interior = tv0 * 8 > s.lo && (tv0 + kSCtaVecs) * 8 < s.hi;
+
+  uint4 v[kSV];
+  uint32_t halo = 0;
+  if (interior) {
+    const uint4* src = s.in + v0;
+#pragma unroll
+    for (int k = 0; k < kSV; k++) v[k] = ld_stream(src + k * 32);
+    const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
+    if (lane == 0) halo = src16[-1];
+    if (lane == 31) halo = src16[(kSV - 1) * 32 * 8 + 8];
+  } else {
+#pragma unroll
+    for (int k = 0; k < kSV; k++) {
+      const uint64_t vi = v0 + k * 32;
+      v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
+    }
+    if (lane == 0) halo = unit_at(s, static_cast<int64_t>(wv0 * 8) - 1);
+    if (lane == 31) halo = unit_at(s, static_cast<int64_t>((wv0 + kSWarpVecs) * 8));
+  }
+
+  // String starts in this warp tile [A0, A1) and whether one starts at A1.
+  const int64_t A0 = static_cast<int64_t>(wv0 * 8) - phase;
+  const int64_t A1 = A0 + kSWarpVecs * 8;
+  uint64_t M = 0;
+  bool start_after = false;
+  for (uint64_t scan = tile_first[tile];; scan += 32) {
+    const uint64_t idx = scan + lane;
+    const int64_t p = idx < count ? __ldg(offsets + idx) : INT64_MAX;
+    uint32_t inr = __ballot_sync(kFull, p >= A0 && p < A1);
+    start_after |= __ballot_sync(kFull, p == A1) != 0;
+    while (inr) {
+      const int j = __ffs(inr) - 1;
+      inr &= inr - 1;
+      const uint32_t r = static_cast<uint32_t>(__shfl_sync(kFull, p, j) - A0);
+      if (lane == static_cast<int>((r >> 3) & 31)) M |= 1ull << (((r >> 8) << 3) | (r & 7));
+    }
+    if (__ballot_sync(kFull, p <= A1) != kFull) break;
+  }
+  if (!interior) {
+#pragma unroll
+    for (int k = 0; k < kSV; k++) {
+      const uint64_t vi = v0 + k * 32;
+      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, v[k]);
+    }
+  }
+  uint32_t F = 0;
+#pragma unroll
+  for (int k = 0; k < kSV; k++) F |= static_cast<uint32_t>((M >> (8 * k)) & 1u) << k;
+  const uint32_t Fd = __shfl_sync(kFull, F, (lane + 1) & 31);
+  const uint32_t after = lane == 31 ? ((Fd >> 1) | (start_after ? (1u << (kSV - 1)) : 0u)) : Fd;
+
+  Flags cur = classify8(v[0]);
+  uint32_t hp_carry = hflag_hi(halo);
+  const uint32_t halo_l = lflag_lo(halo);
+#pragma unroll
+  for (int k = 0; k < kSV; k++) {
+    Flags nxt;
+    if (k + 1 < kSV) nxt = classify8(v[k + 1]);
+    const uint32_t up = __shfl_sync(kFull, cur.H1, (lane + 31) & 31);
+    const uint32_t dn = __shfl_sync(kFull, cur.L0, (lane + 1) & 31);
+    uint32_t ln = dn;
+    if (k + 1 < kSV) {
+      const uint32_t dn_next = __shfl_sync(kFull, nxt.L0, (lane + 1) & 31);
+      if (lane == 31) ln = dn_next;
+    } else if (lane == 31) {
+      ln = halo_l;
+    }
+    const uint32_t hp = lane ? up : hp_carry;
+    hp_carry = up;
+    const uint32_t bits = static_cast<uint32_t>(M >> (8 * k)) & 0xFFu;
+    uint32_t B0, B1;
+    bad8(cur, hp, ln, B0, B1, spread4(bits), spread4(bits >> 4), ((after >> k) & 1u) << 7);
+    const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
+    const uint64_t vi = v0 + k * 32;
+    if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
+      if (store) st_stream(s.out + vi, blend(v[k], B0, B1));
+    } else if (store && vi < vend) {
+      const uint4 r = blend(v[k], B0, B1);
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const uint64_t a = vi * 8 + j;
+        if (a >= s.lo && a < s.hi) {
+          const uint32_t u = get_unit(r, j);
+          if (!kInPlace || u != get_unit(v[k], j)) s.out_units[a - s.lo] = static_cast<uint16_t>(u);
+        }
+      }
+    }
+    if (k + 1 < kSV) cur = nxt;
+  }
+}
+
+cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64_t* offsets, size_t num_strings,
+                                 uint16_t* out, cudaStream_t stream) {
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
+  const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
+  Span s;
+  s.in = reinterpret_cast<const uint4*>(ia - 2 * ph);
+  s.out = reinterpret_cast<uint4*>(oa - 2 * ph);
+  s.out_units = nullptr;
+  s.lo = s.hi = 0;
+  s.left = s.right = -1;
+  s.left_ptr = s.right_ptr = nullptr;
+  s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
+  constexpr uint64_t kTileUnits = kSCtaVecs * 8;
+  const uint64_t count = static_cast<uint64_t>(num_strings) + 1;
+  const uint64_t ntiles_max = (static_cast<uint64_t>(n_units) + 16) / kTileUnits + 2;
+  uint64_t* table = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&table), ntiles_max * sizeof(uint64_t), stream);
+  if (e != cudaSuccess) return e;
+  tile_first_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(offsets, count, ph, table,
+                                                                                    ntiles_max);
+  note_launch();
+  const unsigned g = static_cast<unsigned>(ntiles_max);
+  const int64_t nn = static_cast<int64_t>(n_units);
+  if (in != out) {
+    batched_tile_kernel<false, 1><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nn);
+  } else {
+    switch (inplace_granularity()) {
+      case 1: batched_tile_kernel<true, 1><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nn); break;
+      default: batched_tile_kernel<true, 2><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nn); break;
+    }
+  }
+  note_launch();
+  e = cudaGetLastError();
+  const cudaError_t f = cudaFreeAsync(table, stream);
+  return e != cudaSuccess ? e : f;
+}
+
 cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
                                   cudaStream_t stream) {
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);

@@ -150,7 +150,7 @@ void to_well_formed_batched(std::span<const char16_t> in, std::span<const std::i
   const auto* i = reinterpret_cast<const uint16_t*>(in.data());
   auto* o = reinterpret_cast<uint16_t*>(out.data());
   if (is_device(i)) {
-    check(u16m_to_well_formed_batched(i, offsets.data(), S, o, nullptr));
+    check(u16m_to_well_formed_batched_n(i, in.size(), offsets.data(), S, o, nullptr));
     sync_default();
     return;
   }
@@ -160,7 +160,7 @@ void to_well_formed_batched(std::span<const char16_t> in, std::span<const std::i
   DeviceBuf d(in.size_bytes()), doff(offsets.size_bytes());
   copy(d.p, i, in.size_bytes(), cudaMemcpyHostToDevice);
   copy(doff.p, offsets.data(), offsets.size_bytes(), cudaMemcpyHostToDevice);
-  check(u16m_to_well_formed_batched(d.as<uint16_t>(), doff.as<int64_t>(), S, d.as<uint16_t>(), nullptr));
+  check(u16m_to_well_formed_batched_n(d.as<uint16_t>(), in.size(), doff.as<int64_t>(), S, d.as<uint16_t>(), nullptr));
   copy(o, d.p, in.size_bytes(), cudaMemcpyDeviceToHost);
 }
 

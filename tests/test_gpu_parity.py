@@ -406,3 +406,30 @@ def test_parts_on_two_streams(P, cuda):
             P.to_well_formed_part(t, out, P._lib.PART_EDGES, lp, rp, stream=s2)
             torch.cuda.synchronize()
             assert (host(out) == e).all(), (n, in_place)
+
+
+def test_batched_entry_without_length(P, cuda, golden):
+    """The north-star batched entry (no buffer length; persistent TMA kernel)
+    and the length-aware one (tile table + one tile per CTA) agree with the
+    oracle, including an offsets[S] beyond n that must be clamped."""
+    meta, _ = golden
+    seqs = list(boundary_sequences(5))
+    data, offsets = concat_with_offsets(seqs)
+    L = P._lib.raw()
+    t = dev(data)
+    o = torch.from_numpy(offsets).cuda()
+    out = torch.empty_like(t)
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.u16m_to_well_formed_batched(t.data_ptr(), o.data_ptr(), o.numel() - 1, out.data_ptr(), s) == 0
+    assert sha(host(out)) == meta["boundary5_sha_out"]
+    out2 = torch.empty_like(t)
+    assert L.u16m_to_well_formed_batched_n(t.data_ptr(), t.numel(), o.data_ptr(), o.numel() - 1,
+                                            out2.data_ptr(), s) == 0
+    assert torch.equal(out, out2)
+    # clamping: claim only the first half of the buffer
+    half = t.numel() // 2
+    keep = dev(np.full(t.numel() - half, 0x7777, np.uint16))
+    buf = torch.cat([t[:half], keep])
+    assert L.u16m_to_well_formed_batched_n(buf.data_ptr(), half, o.data_ptr(), o.numel() - 1, buf.data_ptr(), s) == 0
+    torch.cuda.synchronize()
+    assert (host(buf[half:]) == 0x7777).all()
