@@ -309,16 +309,16 @@ __global__ void __launch_bounds__(kSThreads, 3) batched_stream_kernel(Span s, co
 // register-staged streaming (U16M_PERSIST), so the batched form also runs one
 // 16384-unit tile per CTA. The grid is sized from the caller's buffer length
 // (tiles past offsets[S] exit); a pre-pass scatters, per string, its index
-// into the table of "first string starting in or after tile t", so a CTA
-// finds its strings with two dependent loads (table, then a 32-entry window
-// of offsets per warp) issued after — and overlapping — its 8 data loads.
+// into the table of "first string starting in or after warp tile w", so a
+// warp finds its strings with two dependent loads (table, then a 32-entry
+// window of offsets) issued after — and overlapping — its 8 data loads.
 __global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t count, uint32_t phase,
                                   uint64_t* __restrict__ tile_first, uint64_t ntiles_max) {
   const uint64_t s_idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (s_idx >= count) return;
   const int64_t A = __ldg(offsets);
-  const int64_t base = ((A + phase) / 8) * 8 - phase;  // key of tile 0
-  constexpr int64_t kTileUnits = kSThreads / 32 * kSWarpVecs * 8;
+  const int64_t base = ((A + phase) / 8) * 8 - phase;  // key of warp tile 0
+  constexpr int64_t kTileUnits = kSWarpVecs * 8;        // table granularity: one warp tile
   const int64_t p = __ldg(offsets + s_idx);
   uint64_t t_hi = static_cast<uint64_t>((p - base) / kTileUnits);
   uint64_t t_lo = s_idx ? static_cast<uint64_t>((__ldg(offsets + s_idx - 1) - base) / kTileUnits) + 1 : 0;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   const int64_t A1 = A0 + kSWarpVecs * 8;
   uint64_t M = 0;
   bool start_after = false;
-  for (uint64_t scan = tile_first[tile];; scan += 32) {
+  for (uint64_t scan = tile_first[(wv0 - vbeg) / kSWarpVecs];; scan += 32) {
     const uint64_t idx = scan + lane;
     const int64_t p = idx < count ? __ldg(offsets + idx) : INT64_MAX;
     uint32_t inr = __ballot_sync(kFull, p >= A0 && p < A1);
@@ -460,11 +460,12 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   constexpr uint64_t kTileUnits = kSCtaVecs * 8;
   const uint64_t count = static_cast<uint64_t>(num_strings) + 1;
   const uint64_t ntiles_max = (static_cast<uint64_t>(n_units) + 16) / kTileUnits + 2;
-  uint64_t* table = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&table), ntiles_max * sizeof(uint64_t), stream);
+  const uint64_t nwtiles_max = ntiles_max * (kSThreads / 32);
+  uint64_t* table = nullptr;  // first string starting in or after each warp tile
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&table), nwtiles_max * sizeof(uint64_t), stream);
   if (e != cudaSuccess) return e;
   tile_first_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(offsets, count, ph, table,
-                                                                                    ntiles_max);
+                                                                                    nwtiles_max);
   note_launch();
   const unsigned g = static_cast<unsigned>(ntiles_max);
   const int64_t nn = static_cast<int64_t>(n_units);
