@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   if (tile >= ntiles) return;
   const uint64_t tv0 = vbeg + tile * kSCtaVecs;
   const uint64_t wv0 = tv0 + threadIdx.x / 32 * kSWarpVecs;
+  if (wv0 >= vend) return;  // warp tile past the job (no table entry either)
   const uint64_t v0 = wv0 + lane;
   const bool interior = tv0 * 8 > s.lo && (tv0 + kSCtaVecs) * 8 < s.hi;
 
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   }
 
   // String starts in this warp tile [A0, A1) and whether one starts at A1.
+  // (Every warp tile below vend has a table entry: the pre-pass covers all.)
   const int64_t A0 = static_cast<int64_t>(wv0 * 8) - phase;
   const int64_t A1 = A0 + kSWarpVecs * 8;
   uint64_t M = 0;
