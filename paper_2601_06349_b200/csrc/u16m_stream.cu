@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "u16m_internal.h"
 #include "u16m_repair.cuh"
@@ -445,6 +446,23 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   }
 }
 
+// Stream-ordered workspace comes from the device's default memory pool; keep
+// freed blocks cached in the pool (release threshold = max) so per-call
+// cudaMallocAsync/FreeAsync never go back to the driver.
+static void keep_pool_memory() {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::call_once(once[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  });
+}
+
 cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64_t* offsets, size_t num_strings,
                                  uint16_t* out, cudaStream_t stream) {
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
@@ -464,6 +482,7 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   const uint64_t ntiles_max = (static_cast<uint64_t>(n_units) + 16) / kTileUnits + 2;
   const uint64_t nwtiles_max = ntiles_max * (kSThreads / 32);
   uint64_t* table = nullptr;  // first string starting in or after each warp tile
+  keep_pool_memory();
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&table), nwtiles_max * sizeof(uint64_t), stream);
   if (e != cudaSuccess) return e;
   tile_first_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(offsets, count, ph, table,
