@@ -482,13 +482,7 @@ cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long lo
                                   cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(count_out, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess || n == 0) return e;
-  bool same = false;
-  const Span s = make_span(in, n, nullptr, -1, -1, nullptr, nullptr, &same);
-  ScanArgs sc = kNoScan;
-  sc.count_out = count_out;
-  const uint64_t tiles = tiles_for(s);
-  const uint64_t cap = static_cast<uint64_t>(sm_count_for_current_device()) * 8;
-  return launch<kCount, true, false>(s, kNoBatch, sc, tiles < cap ? tiles : cap, stream);
+  return launch_stream_count(in, n, count_out, stream);
 }
 
 // Exclusive prefix over per-tile counts, one CTA, sequential chunks of 1024.

@@ -35,7 +35,7 @@ constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;  // 2048 vectors = 32 K
 // kCount: add the number of rewritten units to *count (warp reduction, one
 // atomic per warp).
 template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false,
-          int kHint = 0>
+          int kHint = 0, bool kNoStore = false>
 __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count) {
   constexpr int kSWarpVecs = 32 * kSV;
   constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
@@ -127,7 +127,9 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
       if (!interior) mask_outside(s, vi, c0, c1);
       if (vi < vend) counted += __popc(c0) + __popc(c1);
     }
-    if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
+    if (kNoStore) {
+      // validation only (count)
+    } else if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
       if (store) st_hint<kHint % 4>(dst + k * 32, blend<kBE>(v[k], B0, B1));
     } else if (store && vi < vend) {
       const uint4 r = blend<kBE>(v[k], B0, B1);
@@ -654,6 +656,28 @@ cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long lo
   else if (ip) launch_codec_t<true, false>(t, g, count, stream);
   else if (big_endian) launch_codec_t<false, true>(t, g, count, stream);
   else launch_codec_t<false, false>(t, g, count, stream);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// Validation (§8(f-1)): the stream kernel with the count and no stores —
+// 2 B/unit read-only, one tile per CTA.
+cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
+  const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
+  Span s;
+  s.in = reinterpret_cast<const uint4*>(ia - 2 * ph);
+  s.out = nullptr;
+  s.out_units = nullptr;
+  s.lo = ph;
+  s.hi = ph + n;
+  s.left = s.right = -1;
+  s.left_ptr = s.right_ptr = nullptr;
+  s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
+  const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kSCtaVecs - 1) / kSCtaVecs;
+  stream_kernel<false, 1, 8, 4, false, true, 0, true><<<static_cast<unsigned>(ntiles), kSThreads, 0, stream>>>(s, count);
   note_launch();
   return cudaGetLastError();
 }
