@@ -47,6 +47,9 @@ cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long lo
 // buffer of an in-place host job). Same 16-byte phase required.
 cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
                                    bool big_endian, unsigned long long* count, cudaStream_t stream);
+// Keep the device default mempool's freed blocks cached (stream-ordered
+// per-call workspaces stay cheap).
+void keep_pool_memory();
 // Count of units repair would rewrite, read-only stream kernel (adds to *count).
 cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream);
 // Batched form with the buffer length known: tile table pre-pass + one tile

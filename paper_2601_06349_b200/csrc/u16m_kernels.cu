@@ -179,6 +179,14 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
 
   for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
     const uint64_t tile = s.tile_sel == kTilesEdges && w == 1 ? ntiles - 1 : tbase + w;
+    if constexpr (kMode == kEmit) {
+      // Tiles whose rewrites all rank past the limit contribute nothing: skip
+      // them before touching their data (the CLI asks for 10 offsets).
+      if (sc.tile_prefix[tile] >= sc.limit) {
+        if (tile + 1 == ntiles && threadIdx.x == 0) *sc.count_out = sc.limit;
+        continue;
+      }
+    }
     const uint64_t cta_v0 = vbeg + tile * kCtaVecs;
     const uint64_t warp_v0 = cta_v0 + static_cast<uint64_t>(warp) * kWarpVecs;
     // Interior tile: every vector full and both warp-tile halos in range.
@@ -521,6 +529,7 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   const Span s = make_span(in, n, nullptr, -1, -1, nullptr, nullptr, &same);
   const uint64_t tiles = tiles_for(s);
   void* ws = nullptr;
+  keep_pool_memory();
   e = cudaMallocAsync(&ws, tiles * (sizeof(uint32_t) + sizeof(unsigned long long)) + 16, stream);
   if (e != cudaSuccess) return e;
   auto* prefix = static_cast<unsigned long long*>(ws);

@@ -146,9 +146,19 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   }
   }  // tile loop
   if constexpr (kCount) {
+    // CTA-level reduction, one atomic per CTA (per-warp atomics on one
+    // address serialise at the L2 slice).
+    __shared__ uint32_t warp_counts[kSThreads / 32];
 #pragma unroll
     for (int o = 16; o; o >>= 1) counted += __shfl_xor_sync(kFull, counted, o);
-    if (lane == 0 && counted) atomicAdd(count, static_cast<unsigned long long>(counted));
+    if (lane == 0) warp_counts[threadIdx.x / 32] = counted;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long c = 0;
+#pragma unroll
+      for (int w = 0; w < kSThreads / 32; w++) c += warp_counts[w];
+      if (c) atomicAdd(count, c);
+    }
   }
 }
 
@@ -451,7 +461,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
 // Stream-ordered workspace comes from the device's default memory pool; keep
 // freed blocks cached in the pool (release threshold = max) so per-call
 // cudaMallocAsync/FreeAsync never go back to the driver.
-static void keep_pool_memory() {
+void keep_pool_memory() {
   static std::once_flag once[64];
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
