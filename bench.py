@@ -321,6 +321,23 @@ def run_ours(args):
         prepare()
         step_kernel()
     torch.cuda.synchronize()
+    graph = None
+    launches_per_step = None
+    if distributed and not args.no_graph:
+        # The sharded step (interior kernel + side-stream gather + edge kernel)
+        # is captured once into a CUDA graph and replayed: no per-step Python /
+        # launch overhead between the NCCL gather and the two repair kernels.
+        prepare()
+        torch.cuda.synchronize()
+        c0 = P.launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step_kernel()
+        launches_per_step = P.launch_count() - c0
+        for _ in range(2):
+            prepare()
+            graph.replay()
+        torch.cuda.synchronize()
     if distributed:
         dist.barrier()
     torch.cuda.synchronize()
@@ -332,8 +349,12 @@ def run_ours(args):
             prepare()
             ev[i][0].record(stream)
             c0 = P.launch_count()
-            step_kernel()
-            repair_launches += P.launch_count() - c0
+            if graph is not None:
+                graph.replay()
+                repair_launches += launches_per_step
+            else:
+                step_kernel()
+                repair_launches += P.launch_count() - c0
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         if distributed:
@@ -475,6 +496,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the sharded (NCCL halo exchange) step even at N=1 (under torchrun)")
+    ap.add_argument("--no-graph", action="store_true", help="do not capture the sharded step in a CUDA graph")
     ap.add_argument("--csv", default=None,
                     help="also append rows in the reference bench CSV schema (proj/src/bench.cpp:151-163)")
     args = ap.parse_args()
