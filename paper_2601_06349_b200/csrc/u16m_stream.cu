@@ -553,7 +553,7 @@ static int stream_vecs() {
   static const int v = [] {
     const char* e = std::getenv("U16M_STREAM_VECS");
     const int x = e ? std::atoi(e) : kDefaultStreamVecs;
-    return (x == 8 || x == 12 || x == 16) ? x : kDefaultStreamVecs;
+    return (x == 4 || x == 8 || x == 12 || x == 16) ? x : kDefaultStreamVecs;
   }();
   return v;
 }
@@ -723,6 +723,7 @@ cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out,
 
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream) {
   switch (stream_vecs()) {
+    case 4: return launch_stream_v<4, 6>(s, part, stream);
     case 12: return launch_stream_v<12, 3>(s, part, stream);
     case 16: return launch_stream_v<16, 2>(s, part, stream);
     default: return launch_stream_v<8, 4>(s, part, stream);
