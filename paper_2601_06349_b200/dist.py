@@ -139,3 +139,60 @@ def repair_shard(shard: torch.Tensor, out: Optional[torch.Tensor] = None, group=
 
         return _lib.to_well_formed_halo(shard, out, left, right)
     return compute(shard, out, left, right)
+
+
+class PeerHalo:
+    """Zero-collective halo access for one-process-per-GPU sharding.
+
+    Every rank maps its nearest non-empty neighbours' shards once (CUDA IPC:
+    peer memory over NVLink on a multi-GPU box, or the same GPU); a step is
+    then ONE kernel launch per rank (u16m_to_well_formed_halo_ptr) whose two
+    halo units are 2-byte loads straight from the neighbours' memory — no
+    collective inside the step. A neighbour may be repairing its own shard in
+    place at the same moment: the unit read is either its original value or
+    its repaired value, and both give the same decision.
+    The caller must make sure all ranks hold the same generation of the
+    logical buffer (e.g. a barrier after refilling shards); this constructor
+    ends with one.
+
+    Uses torch's CUDA IPC plumbing (torch.multiprocessing.reductions) and
+    all_gather_object, so it works with any backend (NCCL, gloo)."""
+
+    def __init__(self, shard: torch.Tensor, group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        self.shard = shard
+        rebuild, args = reduce_tensor(shard)
+        metas = [None] * world
+        dist.all_gather_object(metas, (args, int(shard.numel())), group=group)
+        self._peers = []  # keep the mapped neighbour tensors alive
+        self.left_ptr = self.right_ptr = 0
+        for r in range(self.rank - 1, -1, -1):
+            if metas[r][1] > 0:
+                t = rebuild(*metas[r][0])
+                self._peers.append(t)
+                self.left_ptr = t.data_ptr() + 2 * (t.numel() - 1)
+                break
+        for r in range(self.rank + 1, world):
+            if metas[r][1] > 0:
+                t = rebuild(*metas[r][0])
+                self._peers.append(t)
+                self.right_ptr = t.data_ptr()
+                break
+        torch.cuda.synchronize(shard.device)
+        dist.barrier(group=group)
+
+    def repair(self, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Repair this rank's shard (in place when out is None)."""
+        from . import _lib
+
+        shard = self.shard
+        out = shard if out is None else out
+        if shard.numel() == 0:
+            return out
+        s = torch.cuda.current_stream(shard.device).cuda_stream if stream is None else stream
+        _lib._check(_lib.raw().u16m_to_well_formed_halo_ptr(shard.data_ptr(), shard.numel(), out.data_ptr(),
+                                                            self.left_ptr or None, self.right_ptr or None, s))
+        return out
