@@ -164,11 +164,14 @@ class PeerHalo:
         self.rank = dist.get_rank(group)
         world = dist.get_world_size(group)
         self.shard = shard
+        self._peers = []  # keep the mapped neighbour tensors alive
+        self.left_ptr = self.right_ptr = 0
+        if world == 1:
+            dist.barrier(group=group)
+            return
         rebuild, args = reduce_tensor(shard)
         metas = [None] * world
         dist.all_gather_object(metas, (args, int(shard.numel())), group=group)
-        self._peers = []  # keep the mapped neighbour tensors alive
-        self.left_ptr = self.right_ptr = 0
         for r in range(self.rank - 1, -1, -1):
             if metas[r][1] > 0:
                 t = rebuild(*metas[r][0])
