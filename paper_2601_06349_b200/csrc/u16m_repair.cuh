@@ -198,30 +198,20 @@ __device__ __forceinline__ uint32_t unit_at(const Span& s, int64_t a) {
   return reinterpret_cast<const uint16_t*>(s.in)[a];
 }
 
-// Unit j (0..7) of a vector; select chains only (no addressing), so a
-// run-time j keeps the vector in registers.
 __device__ __forceinline__ uint32_t get_unit(const uint4& v, int j) {
-  const int wi = j >> 1;
-  const uint32_t w = wi == 0 ? v.x : wi == 1 ? v.y : wi == 2 ? v.z : v.w;
+  const uint32_t w = j < 4 ? (j < 2 ? v.x : v.y) : (j < 6 ? v.z : v.w);
   return (j & 1) ? (w >> 16) : (w & 0xFFFFu);
 }
 
 __device__ __forceinline__ void set_unit(uint4& v, int j, uint32_t u) {
-  const uint32_t sh = (j & 1) * 16;
-  const uint32_t m = 0xFFFFu << sh;
-  const uint32_t val = (u & 0xFFFFu) << sh;
-  const int wi = j >> 1;
-  v.x = wi == 0 ? ((v.x & ~m) | val) : v.x;
-  v.y = wi == 1 ? ((v.y & ~m) | val) : v.y;
-  v.z = wi == 2 ? ((v.z & ~m) | val) : v.z;
-  v.w = wi == 3 ? ((v.w & ~m) | val) : v.w;
+  uint32_t* w = j < 4 ? (j < 2 ? &v.x : &v.y) : (j < 6 ? &v.z : &v.w);
+  *w = (j & 1) ? ((*w & 0x0000FFFFu) | (u << 16)) : ((*w & 0xFFFF0000u) | (u & 0xFFFFu));
 }
 
 // Vector vi straddles or lies outside [lo, hi): substitute out-of-range units
 // (halo values are unit values; the vector is in memory byte order).
 template <bool kBE = false>
 __device__ __forceinline__ void patch_edges(const Span& s, uint64_t vi, uint4& v) {
-#pragma unroll 1
   for (int j = 0; j < 8; j++) {
     const uint64_t a = vi * 8 + j;
     if (a < s.lo || a >= s.hi) set_unit(v, j, to_mem<kBE>(unit_at(s, static_cast<int64_t>(a))));
@@ -230,7 +220,7 @@ __device__ __forceinline__ void patch_edges(const Span& s, uint64_t vi, uint4& v
 
 // Clear the flags of units outside [lo, hi) (edge vectors; counting).
 __device__ __forceinline__ void mask_outside(const Span& s, uint64_t vi, uint32_t& B0, uint32_t& B1) {
-#pragma unroll 1
+#pragma unroll
   for (int j = 0; j < 8; j++) {
     const uint64_t a = vi * 8 + j;
     if (a < s.lo || a >= s.hi) {

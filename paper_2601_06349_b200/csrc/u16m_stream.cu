@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
       if (store) st_hint<kHint % 4>(dst + k * 32, blend<kBE>(v[k], B0, B1));
     } else if (store && vi < vend) {
       const uint4 r = blend<kBE>(v[k], B0, B1);
-#pragma unroll 1  // edge vectors only: keep the code (and i-cache) small
+#pragma unroll
       for (int j = 0; j < 8; j++) {
         const uint64_t a = vi * 8 + j;
         if (a >= s.lo && a < s.hi) {
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kSThreads, 3) batched_stream_kernel(Span s, co
         if (store) st_stream(s.out + vi, blend(v[k], B0, B1));
       } else if (store && vi < vend) {
         const uint4 r = blend(v[k], B0, B1);
-#pragma unroll 1  // edge vectors only: keep the code (and i-cache) small
+#pragma unroll
         for (int j = 0; j < 8; j++) {
           const uint64_t a = vi * 8 + j;
           if (a >= s.lo && a < s.hi) {
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
       if (store) st_stream(s.out + vi, blend(v[k], B0, B1));
     } else if (store && vi < vend) {
       const uint4 r = blend(v[k], B0, B1);
-#pragma unroll 1  // edge vectors only: keep the code (and i-cache) small
+#pragma unroll
       for (int j = 0; j < 8; j++) {
         const uint64_t a = vi * 8 + j;
         if (a >= s.lo && a < s.hi) {
