@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
     if (pv + kSCtaVecs <= vend)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s.in + pv), "r"(kSCtaVecs * 16) : "memory");
   }
-  if (__builtin_expect(interior, 1)) {
+  if (interior) {
     const uint4* src = s.in + v0;
 #pragma unroll
     for (int k = 0; k < kSV; k++) v[k] = ld_hint<kHint / 4>(src + k * 32);
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
     }
     if (kNoStore) {
       // validation only (count)
-    } else if (__builtin_expect(interior, 1) || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
+    } else if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
       if (store) st_hint<kHint % 4>(dst + k * 32, blend<kBE>(v[k], B0, B1));
     } else if (store && vi < vend) {
       const uint4 r = blend<kBE>(v[k], B0, B1);
