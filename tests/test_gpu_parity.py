@@ -433,3 +433,24 @@ def test_batched_entry_without_length(P, cuda, golden):
     assert L.u16m_to_well_formed_batched_n(buf.data_ptr(), half, o.data_ptr(), o.numel() - 1, buf.data_ptr(), s) == 0
     torch.cuda.synchronize()
     assert (host(buf[half:]) == 0x7777).all()
+
+
+def test_batched_other_phase_and_copy(P, cuda):
+    """Batched copy into an output whose 16-byte phase differs from the input
+    (general-kernel path) and into an aligned output (tile kernel)."""
+    rng = np.random.default_rng(41)
+    lens = rng.choice([0, 1, 2, 3, 17, 300, 4095, 20000], 2000)
+    offsets = np.zeros(lens.size + 1, np.int64)
+    offsets[1:] = np.cumsum(lens) + 11
+    offsets[0] = 11
+    data = O.gen_config(1, int(offsets[-1]) + 13, seed=41)
+    e = O.fix_batched(data, offsets)
+    t = dev(data)
+    o = torch.from_numpy(offsets).cuda()
+    for shift in (0, 1, 3, 8):
+        big = torch.full((t.numel() + 16,), 0x1234, dtype=torch.int16, device="cuda")
+        out = big[shift:shift + t.numel()]
+        out.copy_(t)
+        P.to_well_formed_batched(t, o, out=out)
+        got = host(out)
+        assert (got == e).all(), shift
