@@ -50,8 +50,6 @@ cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out,
 // Keep the device default mempool's freed blocks cached (stream-ordered
 // per-call workspaces stay cheap).
 void keep_pool_memory();
-// A/B: the stream kernel with shared-memory-staged loads (cp.async).
-cudaError_t launch_stream_smem(const Span& s, cudaStream_t stream);
 // Count of units repair would rewrite, read-only stream kernel (adds to *count).
 cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream);
 // Batched form with the buffer length known: tile table pre-pass + one tile

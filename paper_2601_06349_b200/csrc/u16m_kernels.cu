@@ -411,7 +411,7 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 // "tma" (TMA-pipelined for everything), "ldg" (register-staged everywhere,
 // including the batched form on persistent warps), "general" (the 4-vector
 // general kernel).
-enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoiceLdg = 3, kChoiceSmem = 4 };
+enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoiceLdg = 3 };
 // (kChoiceGeneral and kChoiceAuto share the register-staged kernel for plain
 // streams; they differ for the batched form.)
 static int kernel_choice() {
@@ -420,7 +420,6 @@ static int kernel_choice() {
     if (e && std::strcmp(e, "tma") == 0) return int(kChoiceTma);
     if (e && std::strcmp(e, "general") == 0) return int(kChoiceGeneral);
     if (e && std::strcmp(e, "ldg") == 0) return int(kChoiceLdg);
-    if (e && std::strcmp(e, "smem") == 0) return int(kChoiceSmem);
     return int(kChoiceAuto);
   }();
   return choice;
@@ -454,9 +453,7 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
     if (part == kTilesInterior) return cudaSuccess;
     return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
   }
-  if ((in == out || same) && choice == kChoiceSmem && part == kTilesAll) return launch_stream_smem(s, stream);
-  if ((in == out || same) && (choice == kChoiceAuto || choice == kChoiceLdg || choice == kChoiceSmem))
-    return launch_stream(s, part, stream);
+  if ((in == out || same) && (choice == kChoiceAuto || choice == kChoiceLdg)) return launch_stream(s, part, stream);
   s.tile_sel = part;
   const uint64_t grid = part == kTilesAll ? ntiles
                         : part == kTilesEdges ? (ntiles < 2 ? ntiles : 2)

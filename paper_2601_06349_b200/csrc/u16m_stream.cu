@@ -670,126 +670,6 @@ cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long lo
   return cudaGetLastError();
 }
 
-// ---- shared-memory-staged variant (A/B: U16M_KERNEL=smem) -------------------
-// Same tile and rolling stencil as stream_kernel, but each thread's 8 loads
-// are 16-byte cp.async copies into its own shared-memory slots: in-flight
-// data lives in shared memory (32 KiB per CTA, up to 6 CTAs/SM = 192 KiB per
-// SM) instead of registers (128 KiB per SM). Each thread reads back only what
-// it copied, so cp.async.wait_all is the only synchronisation.
-__device__ __forceinline__ void cp_async16_cg(uint32_t smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ uint4 lds128_u32(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-  return v;
-}
-
-template <bool kInPlace, int kGran>
-__global__ void __launch_bounds__(kSThreads, 6) stream_smem_kernel(Span s) {
-  extern __shared__ __align__(16) unsigned char tile_smem[];
-  const int lane = threadIdx.x & 31;
-  const uint32_t lane_off = threadIdx.x / 32 * kSWarpVecs + lane;
-  const uint64_t vbeg = s.lo / 8;
-  const uint64_t vend = (s.hi + 7) / 8;
-  const uint64_t tile = blockIdx.x;
-  const uint64_t tv0 = vbeg + tile * kSCtaVecs;
-  const bool interior = tv0 * 8 > s.lo && (tv0 + kSCtaVecs) * 8 < s.hi;
-  const uint64_t v0 = tv0 + lane_off;
-  const uint32_t slot0 = static_cast<uint32_t>(__cvta_generic_to_shared(tile_smem)) + lane_off * 16;
-
-#pragma unroll
-  for (int k = 0; k < kSV; k++)
-    if (interior || v0 + k * 32 < vend) cp_async16_cg(slot0 + k * 512, s.in + v0 + k * 32);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  if (s.prefetch_tiles > 0 && threadIdx.x == 0) {
-    const uint64_t pv = tv0 + static_cast<uint64_t>(s.prefetch_tiles) * kSCtaVecs;
-    if (pv + kSCtaVecs <= vend)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s.in + pv), "r"(kSCtaVecs * 16) : "memory");
-  }
-  uint32_t halo = 0;
-  const uint64_t warp_v0 = v0 - lane;
-  if (lane == 0) halo = unit_at(s, static_cast<int64_t>(warp_v0 * 8) - 1);
-  if (lane == 31) halo = unit_at(s, static_cast<int64_t>((warp_v0 + kSWarpVecs) * 8));
-  asm volatile("cp.async.wait_all;" ::: "memory");
-
-  auto fetch = [&](int k) {
-    uint4 v = lds128_u32(slot0 + k * 512);
-    if (!interior) {
-      const uint64_t vi = v0 + k * 32;
-      if (vi >= vend) v = make_uint4(0, 0, 0, 0);
-      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, v);
-    }
-    return v;
-  };
-  uint4 vc = fetch(0);
-  Flags cur = classify8(vc);
-  uint32_t hp_carry = hflag_hi(halo);
-  const uint32_t halo_l = lflag_lo(halo);
-  uint4* dst = s.out + v0;
-#pragma unroll
-  for (int k = 0; k < kSV; k++) {
-    uint4 vn;
-    Flags nxt;
-    if (k + 1 < kSV) {
-      vn = fetch(k + 1);
-      nxt = classify8(vn);
-    }
-    const uint32_t up = __shfl_sync(kFull, cur.H1, (lane + 31) & 31);
-    const uint32_t dn = __shfl_sync(kFull, cur.L0, (lane + 1) & 31);
-    uint32_t ln = dn;
-    if (k + 1 < kSV) {
-      const uint32_t dn_next = __shfl_sync(kFull, nxt.L0, (lane + 1) & 31);
-      if (lane == 31) ln = dn_next;
-    } else if (lane == 31) {
-      ln = halo_l;
-    }
-    const uint32_t hp = lane ? up : hp_carry;
-    hp_carry = up;
-    uint32_t B0, B1;
-    bad8(cur, hp, ln, B0, B1);
-    const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
-    const uint64_t vi = v0 + k * 32;
-    if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
-      if (store) st_stream(dst + k * 32, blend(vc, B0, B1));
-    } else if (store && vi < vend) {
-      const uint4 r = blend(vc, B0, B1);
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const uint64_t a = vi * 8 + j;
-        if (a >= s.lo && a < s.hi) {
-          const uint32_t u = get_unit(r, j);
-          if (!kInPlace || u != get_unit(vc, j)) s.out_units[a - s.lo] = static_cast<uint16_t>(u);
-        }
-      }
-    }
-    if (k + 1 < kSV) {
-      vc = vn;
-      cur = nxt;
-    }
-  }
-}
-
-cudaError_t launch_stream_smem(const Span& s0, cudaStream_t stream) {
-  Span s = s0;
-  const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kSCtaVecs - 1) / kSCtaVecs;
-  if (ntiles == 0) return cudaSuccess;
-  constexpr int kSmem = kSCtaVecs * 16;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(stream_smem_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaFuncSetAttribute(stream_smem_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  });
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  s.prefetch_tiles = ntiles > static_cast<uint64_t>(2 * sms * 6) ? sms * 6 : 0;
-  const unsigned g = static_cast<unsigned>(ntiles);
-  if (s.in != s.out) stream_smem_kernel<false, 1><<<g, kSThreads, kSmem, stream>>>(s);
-  else stream_smem_kernel<true, 2><<<g, kSThreads, kSmem, stream>>>(s);
-  note_launch();
-  return cudaGetLastError();
-}
-
 // Validation (§8(f-1)): the stream kernel with the count and no stores —
 // 2 B/unit read-only, one tile per CTA.
 cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream) {

@@ -18,7 +18,6 @@ VARIANTS = [
     {"U16M_GRAN": "4"},
     {"U16M_GRAN": "8"},
     {"U16M_KERNEL": "ldg"},
-    {"U16M_KERNEL": "smem"},
     {"U16M_KERNEL": "ldg", "U16M_GRAN": "1"},
     {"U16M_GRAN": "4", "U16M_PIPE_CHUNK_KIB": "64"},
     {"U16M_HOST_MODE": "writeback", "U16M_PIPE_CHUNK_KIB": "64"},
