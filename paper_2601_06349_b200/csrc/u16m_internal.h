@@ -57,9 +57,7 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
 bool batched_tiles_enabled();
 cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64_t* offsets, size_t num_strings,
                                  uint16_t* out, cudaStream_t stream);
-// Batched form on persistent warps with the rolling register pipeline.
-cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
-                                  cudaStream_t stream);
+
 
 // §8(f-3): byte-order-aware repair + replacement count (same 16-byte phase).
 // left/right: halo UNIT values (byte order already resolved), -1 = outside.

@@ -408,9 +408,9 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 // copy, config 1 in 133 us), the batched form runs the TMA-pipelined kernel
 // (its producer warp walks the offsets off the consumers' critical path).
 // U16M_KERNEL overrides for A/B runs (profiles/README.md has the numbers):
-// "tma" (TMA-pipelined for everything), "ldg" (register-staged everywhere,
-// including the batched form on persistent warps), "general" (the 4-vector
-// general kernel).
+// "tma" (TMA-pipelined for everything), "ldg" (register-staged everywhere;
+// the length-less batched entry then uses the general kernel), "general"
+// (the 4-vector general kernel for everything).
 enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoiceLdg = 3 };
 // (kChoiceGeneral and kChoiceAuto share the register-staged kernel for plain
 // streams; they differ for the batched form.)
@@ -566,7 +566,6 @@ cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t nu
   const bool same16 = ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
   if ((kernel_choice() == kChoiceTma || kernel_choice() == kChoiceAuto) && same16)
     return launch_batched_tma(in, offsets, num_strings, out, stream);
-  if (kernel_choice() == kChoiceLdg && same16) return launch_batched_stream(in, offsets, num_strings, out, stream);
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
   const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);

@@ -162,161 +162,6 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   }
 }
 
-// ---- batched (CSR) form ---------------------------------------------------
-// Persistent warps, each owning a contiguous chain of 4 KiB warp tiles of the
-// flat range [offsets[0], offsets[S]). A warp searches `offsets` once (32-ary
-// warp search) for its chain start and then walks forward: per tile it loads
-// one 32-entry window of offsets together with the tile's 8 data vectors, so
-// the window latency hides under the data loads. String starts become a
-// per-lane 64-bit mask (bit 8k+j: unit j of vector k starts a string), which
-// feeds the same stencil with "no predecessor at a start, no successor before
-// a start".
-__device__ __forceinline__ uint64_t warp_lb(const int64_t* off, uint64_t count, int64_t key, int lane) {
-  uint64_t lo = 0, hi = count;
-  while (hi - lo > 32) {
-    const uint64_t step = (hi - lo + 31) / 32;
-    const uint64_t idx = lo + static_cast<uint64_t>(lane) * step;
-    const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
-    const uint32_t m = __ballot_sync(kFull, pred);
-    if (m == 0) {
-      lo = lo + 31 * step + 1;
-    } else {
-      const int f = __ffs(m) - 1;
-      if (f == 0) {
-        hi = lo;
-      } else {
-        const uint64_t nlo = lo + static_cast<uint64_t>(f - 1) * step + 1;
-        const uint64_t cand = lo + static_cast<uint64_t>(f) * step;
-        hi = cand < hi ? cand : hi;
-        lo = nlo;
-      }
-    }
-  }
-  const uint64_t idx = lo + lane;
-  const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
-  const uint32_t m = __ballot_sync(kFull, pred);
-  return m ? lo + (__ffs(m) - 1) : hi;
-}
-
-template <bool kInPlace, int kGran>
-__global__ void __launch_bounds__(kSThreads, 3) batched_stream_kernel(Span s, const int64_t* __restrict__ offsets,
-                                                                      uint64_t count, uint32_t phase) {
-  const int lane = threadIdx.x & 31;
-  {
-    const int64_t A = __ldg(offsets), B = __ldg(offsets + count - 1);
-    s.lo = static_cast<uint64_t>(A) + phase;
-    s.hi = static_cast<uint64_t>(B) + phase;
-    s.out_units = reinterpret_cast<uint16_t*>(s.out) + s.lo;
-  }
-  if (s.hi <= s.lo) return;
-  const uint64_t vbeg = s.lo / 8;
-  const uint64_t vend = (s.hi + 7) / 8;
-  const uint64_t nwt = (vend - vbeg + kSWarpVecs - 1) / kSWarpVecs;
-  const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * (kSThreads / 32) + threadIdx.x / 32;
-  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (kSThreads / 32);
-  const uint64_t t0 = nwt * gw / nw, t1 = nwt * (gw + 1) / nw;
-  if (t0 >= t1) return;
-
-  // aligned unit a <-> absolute index a - phase
-  uint64_t sidx = warp_lb(offsets, count, static_cast<int64_t>((vbeg + t0 * kSWarpVecs) * 8) - phase, lane);
-  uint32_t hp_carry = 0;
-  if (lane == 0) hp_carry = hflag_hi(unit_at(s, static_cast<int64_t>((vbeg + t0 * kSWarpVecs) * 8) - 1));
-
-  for (uint64_t t = t0; t < t1; t++) {
-    const uint64_t wv0 = vbeg + t * kSWarpVecs;  // first vector of this warp tile
-    const uint64_t v0 = wv0 + lane;
-    const bool interior = wv0 * 8 >= s.lo && (wv0 + kSWarpVecs) * 8 <= s.hi;
-    uint4 v[kSV];
-    if (interior) {
-#pragma unroll
-      for (int k = 0; k < kSV; k++) v[k] = ld_stream(s.in + v0 + k * 32);
-    } else {
-#pragma unroll
-      for (int k = 0; k < kSV; k++) {
-        const uint64_t vi = v0 + k * 32;
-        v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
-      }
-    }
-    uint32_t tail = 0;  // the unit after this warp tile (lane 31)
-    if (lane == 31) tail = unit_at(s, static_cast<int64_t>((wv0 + kSWarpVecs) * 8));
-    // String starts in [A0, A0 + 2048] (aligned coordinates; the last one is
-    // the unit after the tile).
-    const int64_t A0 = static_cast<int64_t>(wv0 * 8) - phase;
-    const int64_t A1 = A0 + kSWarpVecs * 8;
-    uint64_t M = 0;
-    bool start_after = false;
-    uint64_t scan = sidx, next = sidx;
-    for (;;) {
-      const uint64_t idx = scan + lane;
-      const int64_t p = idx < count ? __ldg(offsets + idx) : INT64_MAX;
-      uint32_t inr = __ballot_sync(kFull, p >= A0 && p < A1);
-      start_after |= __ballot_sync(kFull, p == A1) != 0;
-      next += __popc(__ballot_sync(kFull, p < A1));
-      while (inr) {
-        const int j = __ffs(inr) - 1;
-        inr &= inr - 1;
-        const uint32_t r = static_cast<uint32_t>(__shfl_sync(kFull, p, j) - A0);  // unit within the tile
-        if (lane == static_cast<int>((r >> 3) & 31)) M |= 1ull << (((r >> 8) << 3) | (r & 7));
-      }
-      if (__ballot_sync(kFull, p <= A1) != kFull) break;
-      scan += 32;
-    }
-    sidx = next;
-    if (!interior) {
-#pragma unroll
-      for (int k = 0; k < kSV; k++) {
-        const uint64_t vi = v0 + k * 32;
-        if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, v[k]);
-      }
-    }
-    // start flag of the unit after each vector: lane l+1's first unit of the
-    // same k, or lane 0's first unit of k+1 (lane 31); the tile's tail for k=7.
-    uint32_t F = 0;
-#pragma unroll
-    for (int k = 0; k < kSV; k++) F |= static_cast<uint32_t>((M >> (8 * k)) & 1u) << k;
-    const uint32_t Fd = __shfl_sync(kFull, F, (lane + 1) & 31);
-    const uint32_t after = lane == 31 ? ((Fd >> 1) | (start_after ? (1u << (kSV - 1)) : 0u)) : Fd;
-
-    Flags cur = classify8(v[0]);
-    const uint32_t tail_l = lflag_lo(tail);
-#pragma unroll
-    for (int k = 0; k < kSV; k++) {
-      Flags nxt;
-      if (k + 1 < kSV) nxt = classify8(v[k + 1]);
-      const uint32_t up = __shfl_sync(kFull, cur.H1, (lane + 31) & 31);
-      const uint32_t dn = __shfl_sync(kFull, cur.L0, (lane + 1) & 31);
-      uint32_t ln = dn;
-      if (k + 1 < kSV) {
-        const uint32_t dn_next = __shfl_sync(kFull, nxt.L0, (lane + 1) & 31);
-        if (lane == 31) ln = dn_next;
-      } else if (lane == 31) {
-        ln = tail_l;
-      }
-      const uint32_t hp = lane ? up : hp_carry;
-      hp_carry = up;
-      const uint32_t bits = static_cast<uint32_t>(M >> (8 * k)) & 0xFFu;
-      uint32_t B0, B1;
-      bad8(cur, hp, ln, B0, B1, spread4(bits), spread4(bits >> 4), ((after >> k) & 1u) << 7);
-      const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
-      const uint64_t vi = v0 + k * 32;
-      if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
-        if (store) st_stream(s.out + vi, blend(v[k], B0, B1));
-      } else if (store && vi < vend) {
-        const uint4 r = blend(v[k], B0, B1);
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-          const uint64_t a = vi * 8 + j;
-          if (a >= s.lo && a < s.hi) {
-            const uint32_t u = get_unit(r, j);
-            if (!kInPlace || u != get_unit(v[k], j)) s.out_units[a - s.lo] = static_cast<uint16_t>(u);
-          }
-        }
-      }
-      if (k + 1 < kSV) cur = nxt;
-    }
-  }
-}
-
 // ---- batched form, non-persistent (buffer length known) ----------------------
 // Persistent grids measured 15-20 % slower than one-tile-per-CTA grids for
 // register-staged streaming (U16M_PERSIST), so the batched form also runs one
@@ -516,36 +361,6 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   return e != cudaSuccess ? e : f;
 }
 
-cudaError_t launch_batched_stream(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
-                                  cudaStream_t stream) {
-  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
-  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
-  const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
-  Span s;
-  s.in = reinterpret_cast<const uint4*>(ia - 2 * ph);
-  s.out = reinterpret_cast<uint4*>(oa - 2 * ph);
-  s.out_units = nullptr;
-  s.lo = s.hi = 0;
-  s.left = s.right = -1;
-  s.left_ptr = s.right_ptr = nullptr;
-  s.tile_sel = kTilesAll;
-  s.prefetch_tiles = 0;
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = static_cast<unsigned>(sms * 3);
-  const uint64_t count = static_cast<uint64_t>(num_strings) + 1;
-  if (in != out) {
-    batched_stream_kernel<false, 1><<<grid, kSThreads, 0, stream>>>(s, offsets, count, ph);
-  } else {
-    switch (inplace_granularity()) {
-      case 1: batched_stream_kernel<true, 1><<<grid, kSThreads, 0, stream>>>(s, offsets, count, ph); break;
-      case 4: batched_stream_kernel<true, 4><<<grid, kSThreads, 0, stream>>>(s, offsets, count, ph); break;
-      default: batched_stream_kernel<true, 2><<<grid, kSThreads, 0, stream>>>(s, offsets, count, ph); break;
-    }
-  }
-  note_launch();
-  return cudaGetLastError();
-}
 
 // Vectors per thread of the stream kernel (U16M_STREAM_VECS: 8, 12 or 16;
 // A/B knob — register-staged bytes in flight per SM vs occupancy).
