@@ -32,8 +32,8 @@ constexpr int kSWarpVecs = 32 * kSV;          // 256 vectors = 4 KiB per warp
 constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;  // 2048 vectors = 32 KiB per CTA
 
 // kBE: units are big-endian in memory (fused byte-order handling, §8(f-3));
-// kCount: add the number of rewritten units to *count (warp reduction, one
-// atomic per warp).
+// kCount: add the number of rewritten units to *count (CTA reduction, one
+// atomic per CTA); kNoStore: validation only; kHint: cache-policy A/B.
 template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false,
           int kHint = 0, bool kNoStore = false>
 __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count) {
