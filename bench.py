@@ -144,20 +144,22 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_repair_fn(kind_pref: str = "reference"):
+def cpu_repair_fn(kind_pref: str = "reference", kernel_name: str | None = None):
     """(kind, fn(in_np, out_np, threads)) for the reference's own code when
-    oracle/_ref is built, else the oracle port."""
+    oracle/_ref is built (its default kernel, or `kernel_name`), else the
+    oracle port."""
     import oracle as O
 
     R = O.ref() if kind_pref == "reference" else None
     if R is not None:
-        kernel = O.ref_default_kernel().encode()
+        kname = kernel_name or O.ref_default_kernel()
+        kernel = kname.encode()
 
         def fn(x, out, threads):
             rc = R.ref_to_well_formed_mt(O._p16(x), x.size, O._p16(out), threads, kernel)
             assert rc == 0
 
-        return "reference", fn, O.ref_default_kernel()
+        return "reference", fn, kname
 
     def fn(x, out, threads):
         if x is out:
@@ -180,14 +182,15 @@ def cpu_workload(config: str, units: int):
     return O.gen_config(cfg, units, seed=seed, shard_len=units if cfg == 4 else 0), None
 
 
-def time_cpu(config: str, units: int, reps: int, warmup: int, budget_s: float):
+def time_cpu(config: str, units: int, reps: int, warmup: int, budget_s: float, kernel_name: str | None = None,
+             threads: int | None = None):
     """Best/mean input GB/s of the CPU repair over `units` of the config."""
     import numpy as np
 
     import oracle as O
 
-    kind, fn, kname = cpu_repair_fn()
-    threads = cpu_threads()
+    kind, fn, kname = cpu_repair_fn(kernel_name=kernel_name)
+    threads = threads or cpu_threads()
     x, offsets = cpu_workload(config, units)
     mode = CONFIGS[config][2]
     out = np.empty_like(x)
@@ -428,6 +431,16 @@ def run_ours(args):
             cpu = {"value": round(r["gbps_best"], 3), "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
                    "sample": f"first {r['units']} units of {args.config} ({r['kernel']}), best of {r['reps']} reps "
                              f"in ~10 s, input restored before every in-place rep"}
+            # The reference's scalar and SIMD paths, 1 thread (its own
+            # methodology, bench.hpp:51) and all threads (harness extension).
+            if r["kind"] == "reference" and mode != "batched":
+                paths = {}
+                for kname in ("scalar", r["kernel"]):
+                    for th in (1, cpu_threads()):
+                        q = time_cpu(args.config, cpu_units if th > 1 else min(cpu_units, 1 << 24), reps=100000,
+                                     warmup=1, budget_s=2.0, kernel_name=kname, threads=th)
+                        paths[f"{kname}_{th}thr"] = round(q["gbps_best"], 3)
+                cpu["paths_gbps"] = paths
         except Exception as e:  # noqa: BLE001
             log("cpu baseline failed:", e)
 
