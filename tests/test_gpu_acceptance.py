@@ -1,0 +1,54 @@
+"""GPU analogues of the reference's acceptance performance criteria
+(proj/tests/acceptance.cpp:162-215, 262-283), on device-resident data:
+* criterion 5: the repair loses at most 25 % throughput at 0.1 % mismatches
+  versus clean input (same generator, seeds 5 and 6 as the reference), and
+  beats the reference's own best CPU kernel on this host;
+* criterion 7: throughput is flat within +-30 % of its median over sizes from
+  2^24 units up (sizes where the launch is not the whole cost)."""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def gbps(P, t, reps=20):
+    out = torch.empty_like(t)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    best = float("inf")
+    for _ in range(reps):
+        P._lib.l2_flush(flush)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        P.to_well_formed(t, out=out)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / 1e3)
+    return 2 * t.numel() / best / 1e9
+
+
+def test_mismatch_degradation_and_cpu_speedup(P, cuda):
+    n = 1 << 26
+    clean = np.frombuffer(P.generate_utf16le(n, 0.001, 0.0, 5), np.int16)
+    dirty = np.frombuffer(P.generate_utf16le(n, 0.001, 0.001, 6), np.int16)
+    tc, td = torch.from_numpy(clean.copy()).cuda(), torch.from_numpy(dirty.copy()).cuda()
+    c = max(gbps(P, tc) for _ in range(2))
+    d = max(gbps(P, td) for _ in range(2))
+    assert abs(d - c) <= 0.25 * c, (c, d)
+    if O.ref() is not None:
+        x = dirty.view(np.uint16)[: 1 << 24].copy()
+        t0 = time.perf_counter()
+        O.ref_to_well_formed(x, O.ref_default_kernel())
+        cpu = 2 * x.size / (time.perf_counter() - t0) / 1e9
+        assert c >= 2 * cpu
+
+
+def test_throughput_flat_over_sizes(P, cuda):
+    x = torch.from_numpy(O.gen_config(0, 1 << 28, seed=0).view(np.int16)).cuda()
+    rates = [gbps(P, x[: 1 << k], reps=10) for k in range(24, 29)]
+    med = float(np.median(rates))
+    assert all(abs(r - med) <= 0.30 * med for r in rates), rates
