@@ -41,7 +41,7 @@ namespace u16m {
 enum Mode : int {
   kCopy = 0,       // out = repair(in)
   kInPlace = 1,    // buf = repair(buf), stores only vectors with a rewrite
-  kCount = 2,      // *count_out += number of units repair would rewrite
+  // 2 was a count mode; counting now runs on the stream kernel (u16m_stream.cu)
   kTileCount = 3,  // tile_counts[tile] = rewrites in that CTA tile
   kEmit = 4        // write ascending rewrite offsets (< limit) using tile prefixes
 };
@@ -53,7 +53,7 @@ struct BatchArgs {
 };
 
 struct ScanArgs {
-  unsigned long long* count_out;    // kCount: total; kEmit: number written
+  unsigned long long* count_out;    // kEmit: number written
   uint32_t* tile_counts;            // kTileCount output
   const unsigned long long* tile_prefix;  // kEmit input (exclusive prefix per tile)
   unsigned long long* offsets_out;  // kEmit output
@@ -166,7 +166,6 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
   const uint64_t vbeg = s.lo / 8;
   const uint64_t vend = (s.hi + 7) / 8;
   const uint64_t ntiles = (vend - vbeg + kCtaVecs - 1) / kCtaVecs;
-  uint64_t counted = 0;
   const uint32_t lane_off = static_cast<uint32_t>(warp * kWarpVecs + lane);  // vector offset in tile
   // Tile selection: all tiles, only the two edge tiles, or only the interior
   // tiles (the last two let a caller overlap a halo exchange with the body).
@@ -250,7 +249,7 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
     }
     uint32_t B0[kVecs], B1[kVecs];
     tile_bad<kBatched>(f, halo, lane, starts, (lane_off - lane) * 8, B0, B1);
-    if constexpr (kMode >= kCount) {
+    if constexpr (kMode >= kTileCount) {
 #pragma unroll
       for (int k = 0; k < kVecs; k++)
         if (edge[k]) mask_outside(s, warp_v0 + k * 32 + lane, B0[k], B1[k]);
@@ -278,9 +277,6 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
           }
         }
       }
-    } else if constexpr (kMode == kCount) {
-#pragma unroll
-      for (int k = 0; k < kVecs; k++) counted += __popc(B0[k]) + __popc(B1[k]);
     } else {
       // Rank of each vector's rewrites inside the tile, in unit order
       // (warp-major, then k, then lane).
@@ -333,11 +329,6 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
     }
   }
 
-  if constexpr (kMode == kCount) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) counted += __shfl_xor_sync(kFull, counted, o);
-    if (lane == 0 && counted) atomicAdd(sc.count_out, static_cast<unsigned long long>(counted));
-  }
 }
 
 // ---- host launchers --------------------------------------------------------
