@@ -283,7 +283,13 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
     hp_carry = up;
     const uint32_t bits = static_cast<uint32_t>(M >> (8 * k)) & 0xFFu;
     uint32_t B0, B1;
-    bad8(cur, hp, ln, B0, B1, spread4(bits), spread4(bits >> 4), ((after >> k) & 1u) << 7);
+    const uint32_t aft = (after >> k) & 1u;
+    // Most vectors of a warp hold no string start: skip the start-flag
+    // algebra when no lane needs it (warp-uniform branch).
+    if (__any_sync(kFull, (bits | aft) != 0))
+      bad8(cur, hp, ln, B0, B1, spread4(bits), spread4(bits >> 4), aft << 7);
+    else
+      bad8(cur, hp, ln, B0, B1);
     const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
     const uint64_t vi = v0 + k * 32;
     if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
