@@ -142,7 +142,11 @@ HostPipe* pipe_for(int device, u16m_status* st) {
 //              into host memory (no D2H copy)                          36.0 / —
 //   zerocopy: the kernel reads and writes mapped host buffers directly  36.4 / 38.5
 // Small posted PCIe writes from SMs cost more than a full-duplex DMA copy, so
-// the copy-engine pipeline stays the default.
+// the copy-engine pipeline stays the default. Also measured and dropped:
+// write-back at 64/128/256/512-byte groups (40.8/36.7/37.0/36.9 in place),
+// chunks of 4/8/12/16/24/64 MiB (34-40 in place; ~20 us fixed cost per
+// chunk), and a geometric ramp of the end chunks (no change: fill and drain
+// are not the loss).
 enum HostMode { kHostStaged = 0, kHostWriteback = 1, kHostZeroCopy = 2 };
 int host_mode() {
   static const int m = [] {
