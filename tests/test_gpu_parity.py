@@ -208,6 +208,42 @@ def test_batched_edges(P, cuda):
     assert (got[:5] == data[:5]).all() and (got[offsets[-1]:] == data[offsets[-1]:]).all()
 
 
+def test_batched_tile_records(P, cuda):
+    """Batched starts around the 2048-unit warp-tile records: starts exactly
+    on tile boundaries (the start-after flag), 14-17 starts in one tile (the
+    15-slot record and its overflow scan), strings spanning empty tiles,
+    empty strings on boundaries, every buffer phase."""
+    rng = np.random.default_rng(44)
+    T = 2048
+    for ph in range(8):
+        for first in (0, 1, 7, 13):
+            lens = []
+            pos = first
+            base = (first + ph) // 8 * 8 - ph   # warp tile 0 starts here
+            while pos < 40 * T:
+                kind = rng.integers(0, 6)
+                if kind == 0:      # run to the next tile boundary (relative to base)
+                    lens.append(int(T - (pos - base) % T))
+                elif kind == 1:    # many tiny strings in one tile
+                    lens += [int(rng.integers(0, 3)) for _ in range(int(rng.integers(13, 19)))]
+                elif kind == 2:    # spans several tiles
+                    lens.append(int(rng.integers(2, 5)) * T + int(rng.integers(-2, 3)))
+                elif kind == 3:    # empty strings on a boundary
+                    lens += [int(T - (pos - base) % T), 0, 0]
+                else:
+                    lens.append(int(rng.integers(1, 3000)))
+                pos = first + sum(lens)
+            offs = np.concatenate([[first], first + np.cumsum(lens)]).astype(np.int64)
+            buf = rng.choice(ALPHABET, int(offs[-1]) + ph + 9)
+            data = buf[ph:]
+            e = O.fix_batched(data, offs)
+            t = dev(buf)[ph:]
+            got = host(P.to_well_formed_batched(t, torch.from_numpy(offs).cuda()))
+            assert (got == e).all(), (ph, first)
+            P.to_well_formed_batched(t, torch.from_numpy(offs).cuda(), out=t)
+            assert (host(t) == e).all(), (ph, first, "in place")
+
+
 def test_errors(P, cuda):
     t = torch.zeros(100, dtype=torch.int16, device="cuda")
     with pytest.raises(ValueError):
