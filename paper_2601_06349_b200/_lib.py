@@ -16,7 +16,9 @@ from typing import Optional, Sequence
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libu16m.so")
+# U16M_LIBRARY: load another build of the same ABI (same-box A/B of kernel
+# versions, scripts/ab_lib.sh); the default is the in-tree build.
+_LIB_PATH = os.environ.get("U16M_LIBRARY") or os.path.join(_PKG, "libu16m.so")
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(

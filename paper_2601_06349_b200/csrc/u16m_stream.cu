@@ -166,29 +166,48 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
 // Persistent grids measured 15-20 % slower than one-tile-per-CTA grids for
 // register-staged streaming (U16M_PERSIST), so the batched form also runs one
 // 16384-unit tile per CTA. The grid is sized from the caller's buffer length
-// (tiles past offsets[S] exit); a pre-pass scatters, per string, its index
-// into the table of "first string starting in or after warp tile w", so a
-// warp finds its strings with two dependent loads (table, then a 32-entry
-// window of offsets) issued after — and overlapping — its 8 data loads.
+// (tiles past offsets[S] exit). A pre-pass records, for every warp tile
+// (2048 units) that holds a string start, the index of its first string; a
+// warp finds its strings with two dependent loads (that entry, then a
+// 32-entry window of offsets) issued after — and overlapping — its 8 data
+// loads. The table is first memset to kNoStart and the pre-pass writes only
+// the tiles that hold a start, so a string spanning many tiles costs it
+// nothing (a serial per-string fill made one 2^28-unit string 7x slower
+// than the plain repair); a warp on a start-less tile only checks whether
+// the next tile's first string starts exactly at its end.
+constexpr int kFirstPerThread = 4;
+constexpr uint64_t kNoStart = ~0ull;
+
 __global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t count, uint32_t phase,
-                                  uint64_t* __restrict__ tile_first, uint64_t ntiles_max) {
-  const uint64_t s_idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (s_idx >= count) return;
+                                  uint64_t* __restrict__ tile_first, uint64_t nwt) {
+  const uint64_t s0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * kFirstPerThread;
+  if (s0 >= count) return;
   const int64_t A = __ldg(offsets);
   const int64_t base = ((A + phase) / 8) * 8 - phase;  // key of warp tile 0
-  constexpr int64_t kTileUnits = kSWarpVecs * 8;        // table granularity: one warp tile
-  const int64_t p = __ldg(offsets + s_idx);
-  uint64_t t_hi = static_cast<uint64_t>((p - base) / kTileUnits);
-  uint64_t t_lo = s_idx ? static_cast<uint64_t>((__ldg(offsets + s_idx - 1) - base) / kTileUnits) + 1 : 0;
-  if (t_hi >= ntiles_max) t_hi = ntiles_max - 1;
-  for (uint64_t t = t_lo; t <= t_hi; t++) tile_first[t] = s_idx;
+  constexpr int64_t kTileUnits = kSWarpVecs * 8;        // one warp tile
+  // Offsets outside the buffer are a contract error: clamp, never write out of bounds.
+  auto tile_of = [&](int64_t p) -> uint64_t {
+    const uint64_t t = static_cast<uint64_t>(p - base) / kTileUnits;
+    return t < nwt ? t : nwt - 1;
+  };
+  int64_t p[kFirstPerThread + 1];
+  p[0] = s0 ? __ldg(offsets + s0 - 1) : 0;
+#pragma unroll
+  for (int j = 0; j < kFirstPerThread; j++) p[j + 1] = s0 + j < count ? __ldg(offsets + s0 + j) : 0;
+#pragma unroll
+  for (int j = 0; j < kFirstPerThread; j++) {
+    const uint64_t si = s0 + j;
+    if (si >= count) break;
+    const uint64_t t = tile_of(p[j + 1]);
+    if (si == 0 || tile_of(p[j]) != t) tile_first[t] = si;
+  }
 }
 
 template <bool kInPlace, int kGran>
 __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, const int64_t* __restrict__ offsets,
                                                                     uint64_t count, uint32_t phase,
                                                                     const uint64_t* __restrict__ tile_first,
-                                                                    int64_t n_units) {
+                                                                    uint64_t nwt, int64_t n_units) {
   const int lane = threadIdx.x & 31;
   {
     // Clamp to the caller's buffer: offsets beyond it are a contract error,
@@ -232,12 +251,18 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   }
 
   // String starts in this warp tile [A0, A1) and whether one starts at A1.
-  // (Every warp tile below vend has a table entry: the pre-pass covers all.)
   const int64_t A0 = static_cast<int64_t>(wv0 * 8) - phase;
   const int64_t A1 = A0 + kSWarpVecs * 8;
+  // Scan the offsets from this tile's first string; a tile without a start
+  // (kNoStart: inside a long string) scans from the next tile's first string
+  // instead, which only finds whether one starts exactly at A1.
+  const uint64_t wt = (wv0 - vbeg) / kSWarpVecs;
+  const uint64_t c0 = tile_first[wt];
+  const uint64_t c1 = wt + 1 < nwt ? tile_first[wt + 1] : kNoStart;
+  const uint64_t first = c0 != kNoStart ? c0 : (c1 < count ? c1 : count);
   uint64_t M = 0;
   bool start_after = false;
-  for (uint64_t scan = tile_first[(wv0 - vbeg) / kSWarpVecs];; scan += 32) {
+  for (uint64_t scan = first;; scan += 32) {
     const uint64_t idx = scan + lane;
     const int64_t p = idx < count ? __ldg(offsets + idx) : INT64_MAX;
     uint32_t inr = __ballot_sync(kFull, p >= A0 && p < A1);
@@ -348,17 +373,20 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   keep_pool_memory();
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&table), nwtiles_max * sizeof(uint64_t), stream);
   if (e != cudaSuccess) return e;
-  tile_first_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, stream>>>(offsets, count, ph, table,
-                                                                                    nwtiles_max);
+  e = cudaMemsetAsync(table, 0xFF, nwtiles_max * sizeof(uint64_t), stream);  // kNoStart
+  if (e != cudaSuccess) return e;
+  const uint64_t pthreads = (count + kFirstPerThread - 1) / kFirstPerThread;
+  tile_first_kernel<<<static_cast<unsigned>((pthreads + 255) / 256), 256, 0, stream>>>(offsets, count, ph, table,
+                                                                                       nwtiles_max);
   note_launch();
   const unsigned g = static_cast<unsigned>(ntiles_max);
   const int64_t nn = static_cast<int64_t>(n_units);
   if (in != out) {
-    batched_tile_kernel<false, 1><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nn);
+    batched_tile_kernel<false, 1><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nwtiles_max, nn);
   } else {
     switch (inplace_granularity()) {
-      case 1: batched_tile_kernel<true, 1><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nn); break;
-      default: batched_tile_kernel<true, 2><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nn); break;
+      case 1: batched_tile_kernel<true, 1><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nwtiles_max, nn); break;
+      default: batched_tile_kernel<true, 2><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nwtiles_max, nn); break;
     }
   }
   note_launch();

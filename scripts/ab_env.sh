@@ -2,7 +2,7 @@
 # A/B of kernel knobs on one config: VARIANTS is a list of "NAME=VALUE[,NAME=VALUE]" (or "base").
 # Usage: CFG=c1 VARIANTS="base U16M_GRAN=4" bash scripts/ab_env.sh
 mkdir -p gpurun_out
-for rep in 1 2; do
+for rep in $(seq ${REPS:-2}); do
   for v in ${VARIANTS:-base}; do
     envs=""; [ "$v" != base ] && envs=$(echo "$v" | tr ',' ' ')
     out=$(env $envs timeout 300 python bench.py --config ${CFG:-c1} --steps ${STEPS:-20} --warmup 3 --no-cpu --no-e2e 2>/dev/null |

@@ -53,3 +53,33 @@ def test_throughput_flat_over_sizes(P, cuda):
     rates = [gbps(P, x[: 1 << k], reps=10) for k in range(25, 29)]
     med = float(np.median(rates))
     assert all(abs(r - med) <= 0.30 * med for r in rates), rates
+
+
+def _best_ms(P, fn, flush, reps=8):
+    best = float("inf")
+    for _ in range(reps):
+        P._lib.l2_flush(flush)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return best
+
+
+def test_batched_cost_independent_of_string_lengths(P, cuda):
+    """A batch of a few huge strings costs about what the plain repair of the
+    same bytes costs (the tile pre-pass does O(strings) work, not O(tiles)
+    per long string; a serial fill made one 2^28-unit string ~7x slower)."""
+    n = 1 << 28
+    x = torch.from_numpy(O.gen_config(1, n, seed=11).view(np.int16)).cuda()
+    out = torch.empty_like(x)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    plain = _best_ms(P, lambda: P.to_well_formed(x, out=out), flush)
+    for offs in ([0, n], [0, 3, n - 5, n], [0, n // 2, n]):
+        o = torch.tensor(offs, dtype=torch.int64, device="cuda")
+        t = _best_ms(P, lambda: P.to_well_formed_batched(x, o, out=out), flush)
+        assert t < 1.5 * plain, (offs, t, plain)
+        if offs == [0, n]:
+            assert torch.equal(out, P.to_well_formed(x))   # one string == the plain repair
