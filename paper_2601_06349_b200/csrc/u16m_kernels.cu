@@ -60,35 +60,6 @@ struct ScanArgs {
   unsigned long long limit;         // kEmit cap
 };
 
-// First index in [0, count) with off[idx] >= key, or count. Warp-uniform.
-__device__ __forceinline__ uint64_t warp_lower_bound(const int64_t* off, uint64_t count, int64_t key,
-                                                     int lane) {
-  uint64_t lo = 0, hi = count;
-  while (hi - lo > 32) {
-    const uint64_t step = (hi - lo + 31) / 32;
-    const uint64_t idx = lo + static_cast<uint64_t>(lane) * step;
-    const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
-    const uint32_t m = __ballot_sync(kFull, pred);
-    if (m == 0) {
-      lo = lo + 31 * step + 1;
-    } else {
-      const int f = __ffs(m) - 1;
-      if (f == 0) {
-        hi = lo;
-      } else {
-        const uint64_t nlo = lo + static_cast<uint64_t>(f - 1) * step + 1;
-        const uint64_t cand = lo + static_cast<uint64_t>(f) * step;
-        hi = cand < hi ? cand : hi;
-        lo = nlo;
-      }
-    }
-  }
-  const uint64_t idx = lo + lane;
-  const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
-  const uint32_t m = __ballot_sync(kFull, pred);
-  return m ? lo + (__ffs(m) - 1) : hi;
-}
-
 // Marks every string start of this CTA tile in `starts` (bit i = aligned unit
 // cta_v0*8 + i). Warp 0 searches; the CTA synchronises around it.
 __device__ __forceinline__ void mark_string_starts(const BatchArgs& b, uint64_t cta_v0, uint32_t* starts,
@@ -99,7 +70,7 @@ __device__ __forceinline__ void mark_string_starts(const BatchArgs& b, uint64_t 
     __syncwarp();
     const int64_t key_lo = static_cast<int64_t>(cta_v0 * 8) - static_cast<int64_t>(b.phase);
     const int64_t key_hi = key_lo + kCtaUnits;
-    uint64_t sidx = warp_lower_bound(b.offsets, b.count, key_lo, lane);
+    uint64_t sidx = warp_lower_bound(b.offsets, 0, b.count, key_lo, lane);
     for (;;) {
       const uint64_t idx = sidx + lane;
       const int64_t p = idx < b.count ? __ldg(b.offsets + idx) : INT64_MAX;
@@ -109,7 +80,7 @@ __device__ __forceinline__ void mark_string_starts(const BatchArgs& b, uint64_t 
         atomicOr(&starts[bit >> 5], 1u << (bit & 31));
       }
       if (__ballot_sync(kFull, inside) != kFull) break;
-      sidx += 32;
+      sidx = next_offsets_window(b.offsets, b.count, sidx, p, lane);  // skips runs of empty strings
     }
   }
   __syncthreads();

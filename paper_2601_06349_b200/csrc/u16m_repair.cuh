@@ -253,6 +253,71 @@ __device__ __forceinline__ bool group_dirty(bool dirty, int lane) {
   }
 }
 
+// ---- CSR offsets searches (warp-cooperative, warp-uniform results) ----------
+// First index in [lo, hi) with off[idx] >= key, or hi: a 32-ary search, one
+// dependent round of 32 loads per factor of 32.
+__device__ __forceinline__ uint64_t warp_lower_bound(const int64_t* off, uint64_t lo, uint64_t hi, int64_t key,
+                                                     int lane) {
+  while (hi - lo > 32) {
+    const uint64_t step = (hi - lo + 31) / 32;
+    const uint64_t idx = lo + static_cast<uint64_t>(lane) * step;
+    const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
+    const uint32_t m = __ballot_sync(kFull, pred);
+    if (m == 0) {
+      lo = lo + 31 * step + 1;
+    } else {
+      const int f = __ffs(m) - 1;
+      if (f == 0) {
+        hi = lo;
+      } else {
+        const uint64_t nlo = lo + static_cast<uint64_t>(f - 1) * step + 1;
+        const uint64_t cand = lo + static_cast<uint64_t>(f) * step;
+        hi = cand < hi ? cand : hi;
+        lo = nlo;
+      }
+    }
+  }
+  const uint64_t idx = lo + lane;
+  const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
+  const uint32_t m = __ballot_sync(kFull, pred);
+  return m ? lo + (__ffs(m) - 1) : hi;
+}
+
+// First index >= lo with off[idx] > v, or count. Galloping (lane k probes
+// lo + 2^k - 1), then a 32-ary search of the bracket: O(log run) rounds, so a
+// run of a million equal offsets (empty strings) costs a few loads, not a
+// million-entry walk.
+// Out of line: it runs only on runs of empty strings, and inlining it into
+// the tile kernels' scan loops measurably slowed the common path (C3 -1.5 %).
+static __device__ __noinline__ uint64_t skip_equal_offsets(const int64_t* off, uint64_t count, uint64_t lo, int64_t v,
+                                                       int lane) {
+  for (;;) {
+    if (lo >= count) return count;
+    const uint64_t idx = lo + ((1ull << lane) - 1);
+    const bool gt = idx >= count || __ldg(off + idx) > v;
+    const uint32_t m = __ballot_sync(kFull, gt);
+    if (m == 0) {  // 2^31 equal entries: keep galloping
+      lo += 1ull << 31;
+      continue;
+    }
+    const int k = __ffs(m) - 1;
+    const uint64_t blo = k == 0 ? lo : lo + (1ull << (k - 1));
+    uint64_t bhi = lo + (1ull << k) - 1;
+    if (bhi > count) bhi = count;
+    return warp_lower_bound(off, blo, bhi, v + 1, lane);
+  }
+}
+
+// Start of the next 32-entry window of a forward offsets scan whose current
+// window (this lane's entry p) starts at `scan`: scan + 32, or past the whole
+// run when the window holds one repeated value.
+__device__ __forceinline__ uint64_t next_offsets_window(const int64_t* off, uint64_t count, uint64_t scan,
+                                                        int64_t p, int lane) {
+  int same = 0;
+  __match_all_sync(kFull, p, &same);
+  return same ? skip_equal_offsets(off, count, scan + 32, p, lane) : scan + 32;
+}
+
 // 4 bits -> bit 7 of byte lanes 0..3.
 __device__ __forceinline__ uint32_t spread4(uint32_t bits) {
   return (((bits & 0xFu) * 0x00204081u) & 0x01010101u) << 7;

@@ -203,6 +203,25 @@ __global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t 
   }
 }
 
+// String starts of one warp tile [A0, A1): bit 8k+j of lane l's M marks
+// unit A0 + 256k + 8l + j; `after`: a string starts exactly at A1.
+struct StartScan {
+  uint64_t M;
+  bool after;
+};
+
+// Folds one 32-entry window of offsets (this lane's entry p) into st.
+__device__ __forceinline__ void scan_window(int64_t p, int64_t A0, int64_t A1, int lane, StartScan& st) {
+  uint32_t inr = __ballot_sync(kFull, p >= A0 && p < A1);
+  st.after |= __ballot_sync(kFull, p == A1) != 0;
+  while (inr) {
+    const int j = __ffs(inr) - 1;
+    inr &= inr - 1;
+    const uint32_t r = static_cast<uint32_t>(__shfl_sync(kFull, p, j) - A0);
+    if (lane == static_cast<int>((r >> 3) & 31)) st.M |= 1ull << (((r >> 8) << 3) | (r & 7));
+  }
+}
+
 template <bool kInPlace, int kGran>
 __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, const int64_t* __restrict__ offsets,
                                                                     uint64_t count, uint32_t phase,
@@ -260,21 +279,16 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   const uint64_t c0 = tile_first[wt];
   const uint64_t c1 = wt + 1 < nwt ? tile_first[wt + 1] : kNoStart;
   const uint64_t first = c0 != kNoStart ? c0 : (c1 < count ? c1 : count);
-  uint64_t M = 0;
-  bool start_after = false;
-  for (uint64_t scan = first;; scan += 32) {
+  StartScan st{0, false};
+  for (uint64_t scan = first;;) {
     const uint64_t idx = scan + lane;
     const int64_t p = idx < count ? __ldg(offsets + idx) : INT64_MAX;
-    uint32_t inr = __ballot_sync(kFull, p >= A0 && p < A1);
-    start_after |= __ballot_sync(kFull, p == A1) != 0;
-    while (inr) {
-      const int j = __ffs(inr) - 1;
-      inr &= inr - 1;
-      const uint32_t r = static_cast<uint32_t>(__shfl_sync(kFull, p, j) - A0);
-      if (lane == static_cast<int>((r >> 3) & 31)) M |= 1ull << (((r >> 8) << 3) | (r & 7));
-    }
+    scan_window(p, A0, A1, lane, st);
     if (__ballot_sync(kFull, p <= A1) != kFull) break;
+    scan = next_offsets_window(offsets, count, scan, p, lane);  // skips runs of empty strings
   }
+  const uint64_t M = st.M;
+  const bool start_after = st.after;
   if (!interior) {
 #pragma unroll
     for (int k = 0; k < kSV; k++) {

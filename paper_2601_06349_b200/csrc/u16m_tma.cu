@@ -109,34 +109,6 @@ __device__ __forceinline__ void job_range(Span& s, const BatchArgsT& b, bool bat
   }
 }
 
-// 32-ary warp-cooperative lower bound (first idx with off[idx] >= key).
-__device__ __forceinline__ uint64_t lower_bound32(const int64_t* off, uint64_t count, int64_t key, int lane) {
-  uint64_t lo = 0, hi = count;
-  while (hi - lo > 32) {
-    const uint64_t step = (hi - lo + 31) / 32;
-    const uint64_t idx = lo + static_cast<uint64_t>(lane) * step;
-    const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
-    const uint32_t m = __ballot_sync(kFull, pred);
-    if (m == 0) {
-      lo = lo + 31 * step + 1;
-    } else {
-      const int f = __ffs(m) - 1;
-      if (f == 0) {
-        hi = lo;
-      } else {
-        const uint64_t nlo = lo + static_cast<uint64_t>(f - 1) * step + 1;
-        const uint64_t cand = lo + static_cast<uint64_t>(f) * step;
-        hi = cand < hi ? cand : hi;
-        lo = nlo;
-      }
-    }
-  }
-  const uint64_t idx = lo + lane;
-  const bool pred = idx < hi ? (__ldg(off + idx) >= key) : true;
-  const uint32_t m = __ballot_sync(kFull, pred);
-  return m ? lo + (__ffs(m) - 1) : hi;
-}
-
 template <int kInPlace, bool kBatched, int kGran>
 __global__ void __launch_bounds__(kThreadsTma, kTmaCtasPerSm) repair_tma_kernel(Span s, BatchArgsT b) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -174,7 +146,7 @@ __global__ void __launch_bounds__(kThreadsTma, kTmaCtasPerSm) repair_tma_kernel(
     if constexpr (kBatched) {
       if (t_begin < t_end) {
         const int64_t key0 = static_cast<int64_t>((vbeg + t_begin * kCtaVecs) * 8) - static_cast<int64_t>(b.phase);
-        sidx = lower_bound32(b.offsets, b.count, key0, lane);
+        sidx = warp_lower_bound(b.offsets, 0, b.count, key0, lane);
         win = sidx + lane < b.count ? __ldg(b.offsets + sidx + lane) : INT64_MAX;
       }
     }
@@ -208,7 +180,14 @@ __global__ void __launch_bounds__(kThreadsTma, kTmaCtasPerSm) repair_tma_kernel(
           }
           next += __popc(__ballot_sync(kFull, p < key_hi));
           if (__ballot_sync(kFull, inside) != kFull) break;
-          scan += 32;
+          const int64_t p0 = __shfl_sync(kFull, p, 0), p31 = __shfl_sync(kFull, p, 31);
+          if (p0 == p31) {  // a run of equal offsets (empty strings): skip it
+            const uint64_t to = skip_equal_offsets(b.offsets, b.count, scan + 32, p31, lane);
+            if (p31 < key_hi) next += to - (scan + 32);
+            scan = to;
+          } else {
+            scan += 32;
+          }
           p = scan + lane < b.count ? __ldg(b.offsets + scan + lane) : INT64_MAX;
         }
         sidx = next;  // first string starting at or after the next tile's first unit

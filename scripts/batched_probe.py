@@ -30,10 +30,26 @@ def timed(fn, reps=20):
     return ts[len(ts) // 2] * 1e3
 
 
+L = _lib.raw()
+empties = torch.zeros((1 << 20) + 2, dtype=torch.int64, device="cuda")
+empties[-1] = n  # 2^20 empty strings at 0, then one string over the whole buffer
+odd = torch.empty(n + 8, dtype=torch.int16, device="cuda")[3:3 + n]  # out phase != in phase
+
+
+def nolen(offs):  # the length-less entry (no buffer length: TMA producer-walk kernel)
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.u16m_to_well_formed_batched(d.data_ptr(), offs.data_ptr(), offs.numel() - 1, out.data_ptr(), s) == 0
+
+
 for name, fn in [
     ("c3 batch", lambda: _lib.to_well_formed_batched(d, o, out=out)),
     ("one string", lambda: _lib.to_well_formed_batched(d, one, out=out)),
+    ("empties+one", lambda: _lib.to_well_formed_batched(d, empties, out=out)),
+    ("c3 other-phase out", lambda: _lib.to_well_formed_batched(d, o, out=odd)),
+    ("c3 no-length", lambda: nolen(o)),
+    ("one no-length", lambda: nolen(one)),
+    ("empties no-len", lambda: nolen(empties)),
     ("plain copy", lambda: _lib.to_well_formed(d, out=out)),
 ]:
     us = timed(fn)
-    print(f"{os.environ.get('TAG', '')} {name:12s} {us:7.1f} us  {2 * n / us / 1e3:7.1f} GB/s in", flush=True)
+    print(f"{os.environ.get('TAG', '')} {name:20s} {us:7.1f} us  {2 * n / us / 1e3:7.1f} GB/s in", flush=True)

@@ -71,13 +71,16 @@ def _best_ms(P, fn, flush, reps=8):
 def test_batched_cost_independent_of_string_lengths(P, cuda):
     """A batch of a few huge strings costs about what the plain repair of the
     same bytes costs (the tile pre-pass does O(strings) work, not O(tiles)
-    per long string; a serial fill made one 2^28-unit string ~7x slower)."""
+    per long string; a serial fill made one 2^28-unit string ~7x slower),
+    and so does one preceded by a million empty strings (runs of equal
+    offsets are skipped by galloping, not walked: that took 100 ms)."""
     n = 1 << 28
     x = torch.from_numpy(O.gen_config(1, n, seed=11).view(np.int16)).cuda()
     out = torch.empty_like(x)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     plain = _best_ms(P, lambda: P.to_well_formed(x, out=out), flush)
-    for offs in ([0, n], [0, 3, n - 5, n], [0, n // 2, n]):
+    empties = [0] * (1 << 20) + [n]          # a million empty strings, then one huge string
+    for offs in ([0, n], [0, 3, n - 5, n], [0, n // 2, n], empties):
         o = torch.tensor(offs, dtype=torch.int64, device="cuda")
         t = _best_ms(P, lambda: P.to_well_formed_batched(x, o, out=out), flush)
         assert t < 1.5 * plain, (offs, t, plain)

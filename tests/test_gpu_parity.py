@@ -488,3 +488,33 @@ def test_batched_other_phase_and_copy(P, cuda):
         P.to_well_formed_batched(t, o, out=out)
         got = host(out)
         assert (got == e).all(), shift
+
+
+def test_batched_runs_of_empty_strings(P, cuda):
+    """Long runs of equal offsets (empty strings) at the buffer start, on warp
+    and CTA tile boundaries, mid-tile and at the end, through every batched
+    entry: length-aware (tile table), length-less (TMA producer walk),
+    mismatched in/out phase (general kernel) and in place."""
+    rng = np.random.default_rng(77)
+    L = P._lib.raw()
+    s = torch.cuda.current_stream().cuda_stream
+    for run in (1, 31, 32, 33, 100, 5000, 70_000):
+        n = 60_000
+        pts = sorted({0, 2048, 4096, 8192, 16384, 16385, 3001, 40_000, n} | set(int(v) for v in rng.integers(0, n, 20)))
+        offs = []
+        for p in pts:
+            offs += [p] * (run if p in (0, 2048, 16384, 40_000, n) else 1 + int(rng.integers(0, 3)))
+        offs = np.array(offs, np.int64)
+        data = rng.choice(ALPHABET, n + 16)
+        e = O.fix_batched(data, offs)
+        t, o = dev(data), torch.from_numpy(offs).cuda()
+        assert (host(P.to_well_formed_batched(t, o)) == e).all(), ("tiles", run)
+        out = torch.empty_like(t)
+        assert L.u16m_to_well_formed_batched(t.data_ptr(), o.data_ptr(), o.numel() - 1, out.data_ptr(), s) == 0
+        assert (host(out) == e).all(), ("no-length", run)
+        odd = torch.empty(n + 24, dtype=torch.int16, device="cuda")[3:3 + n + 16]
+        P.to_well_formed_batched(t, o, out=odd)
+        assert (host(odd)[: n] == e[: n]).all(), ("other phase", run)
+        u = t.clone()
+        P.to_well_formed_batched(u, o, out=u)
+        assert (host(u) == e).all(), ("in place", run)
