@@ -1,0 +1,351 @@
+// Probe (not product): memory-system ceilings for config 1's access pattern —
+// read every 16-byte vector of a 512 MiB buffer, write back only the 32-byte
+// sectors that hold a surrogate (~40 % of sectors for uniform 16-bit data) —
+// under different kernel structures, with the L2 flushed before every rep.
+// Answers: how far is the stream kernel (131 us on C1) from what the memory
+// system allows for this read/write mix, and which structure gets closest.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 scripts/c1_probe.cu -o scripts/c1_probe
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess) {                                                        \
+      printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__);    \
+      return 1;                                                                     \
+    }                                                                               \
+  } while (0)
+
+__device__ __forceinline__ uint4 ldcs(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stcs(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// any unit of the vector a surrogate (high byte & 0xF8 == 0xD8)
+__device__ __forceinline__ bool has_sur(uint4 v) {
+  uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    uint32_t a = (w[i] & 0xF800F800u) ^ 0xD800D800u;  // 0 in a half <=> surrogate
+    uint32_t lo = a & 0xFFFFu, hi = a >> 16;
+    r |= (lo == 0) | (hi == 0);
+  }
+  return r;
+}
+// sector-dirty: lane pair (2 x 16 B = one 32-byte sector)
+__device__ __forceinline__ bool sector_dirty(bool d, int lane) {
+  const uint32_t m = __ballot_sync(0xFFFFFFFFu, d);
+  return (m >> (lane & ~1)) & 3u;
+}
+
+// one tile per CTA: U vectors per thread, read all, store dirty sectors (kWrite)
+template <int U, int MB, bool kWrite, int kPf>
+__global__ void __launch_bounds__(256, MB) tile_kernel(uint4* buf, size_t nvec, unsigned* sink) {
+  const int lane = threadIdx.x & 31;
+  const size_t tv0 = (size_t)blockIdx.x * 256 * U;
+  const size_t v0 = tv0 + (threadIdx.x / 32) * 32 * U + lane;
+  if (kPf > 0 && threadIdx.x == 0) {
+    const size_t pv = tv0 + (size_t)kPf * 256 * U;
+    if (pv + 256 * U <= nvec)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(buf + pv), "r"(256 * U * 16) : "memory");
+  }
+  uint4 v[U];
+#pragma unroll
+  for (int k = 0; k < U; k++) v[k] = ldcs(buf + v0 + 32 * k);
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < U; k++) {
+    const bool d = sector_dirty(has_sur(v[k]), lane);
+    if (kWrite) {
+      if (d) stcs(buf + v0 + 32 * k, v[k]);
+    } else {
+      acc ^= v[k].x ^ v[k].w ^ (uint32_t)d;
+    }
+  }
+  if (!kWrite && acc == 0x7777777u) *sink = acc;
+}
+
+// persistent, software-pipelined: loads of the next tile issued before the
+// current tile's checks and stores
+template <int U, int MB>
+__global__ void __launch_bounds__(256, MB) pipe_kernel(uint4* buf, size_t nvec) {
+  const int lane = threadIdx.x & 31;
+  const size_t ntiles = nvec / (256 * U);
+  const size_t off = (threadIdx.x / 32) * 32 * U + lane;
+  size_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  uint4 a[U], b[U];
+#pragma unroll
+  for (int k = 0; k < U; k++) a[k] = ldcs(buf + t * 256 * U + off + 32 * k);
+  for (;;) {
+    const size_t tn = t + gridDim.x;
+    if (tn < ntiles) {
+#pragma unroll
+      for (int k = 0; k < U; k++) b[k] = ldcs(buf + tn * 256 * U + off + 32 * k);
+    }
+#pragma unroll
+    for (int k = 0; k < U; k++)
+      if (sector_dirty(has_sur(a[k]), lane)) stcs(buf + t * 256 * U + off + 32 * k, a[k]);
+    if (tn >= ntiles) break;
+#pragma unroll
+    for (int k = 0; k < U; k++) a[k] = b[k];
+    t = tn;
+  }
+}
+
+// TMA ring: one producer thread streams TILE-byte tiles into STAGES smem
+// stages; 8 consumer warps read them (LDS.128) and store dirty sectors.
+template <int STAGES, int TILE>
+__global__ void __launch_bounds__(288) tma_kernel(uint4* buf, size_t nvec, int write) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * TILE);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const size_t ntiles = nvec * 16 / TILE;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; i++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[i])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[i])), "r"(8));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (lane) return;
+    uint32_t it = 0;
+    for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
+      const int st = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      if (it >= STAGES) {
+        uint32_t done;
+        do {
+          asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                       : "=r"(done) : "r"(smem_u32(&empty[st])), "r"(ph ^ 1) : "memory");
+        } while (!done);
+      }
+      const uint32_t fb = smem_u32(&full[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(TILE) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(smem + st * TILE)), "l"((const char*)buf + t * TILE), "r"(TILE), "r"(fb) : "memory");
+    }
+    return;
+  }
+  uint32_t it = 0;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, it++) {
+    const int st = it % STAGES;
+    const uint32_t ph = (it / STAGES) & 1;
+    uint32_t done;
+    do {
+      asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                   : "=r"(done) : "r"(smem_u32(&full[st])), "r"(ph) : "memory");
+    } while (!done);
+    const uint4* s = reinterpret_cast<const uint4*>(smem + st * TILE);
+    uint4* g = buf + t * (TILE / 16);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < TILE / 16; i += 256) {
+      const uint4 v = s[i];
+      if (sector_dirty(has_sur(v), lane) && write) stcs(g + i, v);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+  }
+}
+
+__global__ void fill_kernel(uint32_t* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint64_t z = i * 0x9E3779B97F4A7C15ull + 1;
+    z ^= z >> 31; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 29;
+    p[i] = (uint32_t)(z >> 17);
+  }
+}
+__global__ void flush_kernel(const uint4* p, size_t n16, unsigned* sink) {
+  uint32_t acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) {
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p + i));
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x12345678u) *sink = acc;
+}
+
+// config-0 floor probes (32 MiB copy): whole per-SM share loaded by TMA up
+// front (one CTA per SM, up to kCh chunks in flight), then bulk-stored.
+template <int kCh, int kChunk>
+__global__ void __launch_bounds__(128) share_copy(const uint4* in, uint4* out, size_t nbytes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kCh * kChunk);
+  const size_t share = (nbytes / gridDim.x + 15) / 16 * 16;
+  const size_t b0 = blockIdx.x * share;
+  const size_t b1 = b0 + share < nbytes ? b0 + share : nbytes;
+  if (b0 >= b1) return;
+  const int nch = (int)((b1 - b0 + kChunk - 1) / kChunk);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kCh; i++) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[i])), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    for (int c = 0; c < nch && c < kCh; c++) {
+      const uint32_t len = (uint32_t)min((size_t)kChunk, b1 - b0 - (size_t)c * kChunk);
+      const uint32_t fb = smem_u32(&full[c]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(len) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(smem + c * kChunk)), "l"((const char*)in + b0 + (size_t)c * kChunk), "r"(len), "r"(fb) : "memory");
+    }
+    for (int c = 0; c < nch && c < kCh; c++) {
+      const uint32_t len = (uint32_t)min((size_t)kChunk, b1 - b0 - (size_t)c * kChunk);
+      uint32_t done;
+      do {
+        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                     : "=r"(done) : "r"(smem_u32(&full[c])), "r"(0) : "memory");
+      } while (!done);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"((char*)out + b0 + (size_t)c * kChunk), "r"(smem_u32(smem + c * kChunk)), "r"(len) : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  __syncthreads();
+}
+template <int U>
+__global__ void __launch_bounds__(256) ldg_copy(const uint4* in, uint4* out) {
+  const size_t base = (size_t)blockIdx.x * 256 * U + (threadIdx.x / 32) * 32 * U + (threadIdx.x & 31);
+  uint4 v[U];
+#pragma unroll
+  for (int k = 0; k < U; k++) v[k] = ldcs(in + base + 32 * k);
+#pragma unroll
+  for (int k = 0; k < U; k++) stcs(out + base + 32 * k, v[k]);
+}
+__global__ void empty_kernel() {}
+
+static uint4* g_flush;
+static size_t g_flush_n;
+static unsigned* g_sink;
+
+template <class F>
+static float timeit(F f, int reps = 12) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  std::vector<float> ts;
+  for (int r = 0; r < reps + 2; r++) {
+    flush_kernel<<<148 * 8, 256>>>(g_flush, g_flush_n, g_sink);
+    cudaEventRecord(a);
+    f();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (r >= 2) ts.push_back(ms);
+  }
+  std::sort(ts.begin(), ts.end());
+  return ts[ts.size() / 2];
+}
+
+int main() {
+  const size_t bytes = size_t(1) << 29;  // 2^28 units
+  const size_t nvec = bytes / 16;
+  uint4* d;
+  CK(cudaMalloc(&d, bytes));
+  CK(cudaMalloc(&g_flush, bytes));
+  CK(cudaMalloc(&g_sink, 4));
+  g_flush_n = bytes / 16;
+  fill_kernel<<<148 * 8, 256>>>(reinterpret_cast<uint32_t*>(d), bytes / 4);
+  cudaMemset(g_flush, 1, bytes);
+  CK(cudaDeviceSynchronize());
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  auto rep = [&](const char* name, float ms, bool write) {
+    // DRAM-level bytes: all reads + ~40 % sectors written (printed as input GB/s and read GB/s)
+    printf("%-44s %8.1f us  input %7.1f GB/s  read %7.1f GB/s%s\n", name, ms * 1e3, bytes / ms / 1e6,
+           bytes / ms / 1e6, write ? "  (+ dirty-sector writes)" : "");
+  };
+#define TILE_RUN(U, MB, W, PF)                                                                           \
+  {                                                                                                      \
+    float ms = timeit([&] { tile_kernel<U, MB, W, PF><<<nvec / (256 * U), 256>>>(d, nvec, g_sink); }); \
+    char nm[96];                                                                                         \
+    snprintf(nm, 96, "tile U=%d mb=%d %s pf=%d", U, MB, W ? "inplace" : "read", PF);                     \
+    rep(nm, ms, W);                                                                                      \
+  }
+  TILE_RUN(8, 4, false, 0);
+  TILE_RUN(8, 4, true, 0);
+  TILE_RUN(8, 4, true, 592);
+  TILE_RUN(8, 4, false, 592);
+  TILE_RUN(4, 8, false, 0);
+  TILE_RUN(4, 8, true, 0);
+  TILE_RUN(16, 2, false, 0);
+  TILE_RUN(16, 2, true, 0);
+  TILE_RUN(16, 2, true, 296);
+  TILE_RUN(8, 4, true, 1184);
+  for (int mb : {2, 3, 4}) {
+    float ms;
+    if (mb == 2) ms = timeit([&] { pipe_kernel<8, 2><<<sms * 2, 256>>>(d, nvec); });
+    else if (mb == 3) ms = timeit([&] { pipe_kernel<4, 3><<<sms * 3, 256>>>(d, nvec); });
+    else ms = timeit([&] { pipe_kernel<4, 4><<<sms * 4, 256>>>(d, nvec); });
+    char nm[96];
+    snprintf(nm, 96, "pipe %s", mb == 2 ? "U=8 x2" : mb == 3 ? "U=4 x3" : "U=4 x4");
+    rep(nm, ms, true);
+  }
+#define TMA_RUN(ST, TL, CTAS, W)                                                                         \
+  {                                                                                                      \
+    const size_t sm = (ST) * (TL) + 2 * (ST) * 8;                                                        \
+    cudaFuncSetAttribute(tma_kernel<ST, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);      \
+    float ms = timeit([&] { tma_kernel<ST, TL><<<sms * CTAS, 288, sm>>>(d, nvec, W); });                 \
+    char nm[96];                                                                                         \
+    snprintf(nm, 96, "tma st=%d tile=%d ctas=%d %s", ST, TL, CTAS, W ? "inplace" : "read");              \
+    rep(nm, ms, W);                                                                                      \
+    CK(cudaGetLastError());                                                                              \
+  }
+  TMA_RUN(6, 16384, 2, 0);
+  TMA_RUN(6, 16384, 2, 1);
+  TMA_RUN(12, 16384, 1, 1);
+  TMA_RUN(4, 16384, 3, 1);
+  TMA_RUN(3, 32768, 2, 1);
+  TMA_RUN(6, 32768, 1, 1);
+  TMA_RUN(8, 8192, 3, 1);
+  {
+    uint4* o;
+    CK(cudaMalloc(&o, bytes));
+    float ms = timeit([&] { cudaMemcpyAsync(o, d, bytes, cudaMemcpyDeviceToDevice); });
+    printf("%-44s %8.1f us  r+w %7.1f GB/s\n", "cudaMemcpy D2D", ms * 1e3, 2 * bytes / ms / 1e6);
+  }
+  {
+    const size_t cb = size_t(1) << 25;  // config 0: 32 MiB in, 32 MiB out
+    uint4* o;
+    CK(cudaMalloc(&o, cb));
+    float ms = timeit([&] { empty_kernel<<<1, 32>>>(); });
+    printf("%-44s %8.1f us\n", "c0: empty kernel (event overhead)", ms * 1e3);
+    ms = timeit([&] { cudaMemcpyAsync(o, d, cb, cudaMemcpyDeviceToDevice); });
+    printf("%-44s %8.1f us  input %7.1f GB/s\n", "c0: cudaMemcpy D2D 32 MiB", ms * 1e3, cb / ms / 1e6);
+    ms = timeit([&] { ldg_copy<8><<<cb / (16 * 256 * 8), 256>>>(d, o); });
+    printf("%-44s %8.1f us  input %7.1f GB/s\n", "c0: ldg copy U=8 tile/CTA", ms * 1e3, cb / ms / 1e6);
+    ms = timeit([&] { ldg_copy<4><<<cb / (16 * 256 * 4), 256>>>(d, o); });
+    printf("%-44s %8.1f us  input %7.1f GB/s\n", "c0: ldg copy U=4 tile/CTA", ms * 1e3, cb / ms / 1e6);
+    ms = timeit([&] { ldg_copy<2><<<cb / (16 * 256 * 2), 256>>>(d, o); });
+    printf("%-44s %8.1f us  input %7.1f GB/s\n", "c0: ldg copy U=2 tile/CTA", ms * 1e3, cb / ms / 1e6);
+#define SHARE_RUN(CH, CHUNK, G)                                                                         \
+    {                                                                                                    \
+      const int sm = (CH) * (CHUNK) + (CH) * 8;                                                          \
+      cudaFuncSetAttribute(share_copy<CH, CHUNK>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);      \
+      ms = timeit([&] { share_copy<CH, CHUNK><<<G, 128, sm>>>(d, o, cb); });                             \
+      printf("c0: tma share copy ch=%2d chunk=%6d grid=%4d  %8.1f us  input %7.1f GB/s %s\n", CH, CHUNK, G, \
+             ms * 1e3, cb / ms / 1e6, cudaGetErrorString(cudaGetLastError()));                           \
+    }
+    SHARE_RUN(14, 16384, 148);
+    SHARE_RUN(7, 32768, 148);
+    SHARE_RUN(7, 16384, 296);
+    SHARE_RUN(4, 16384, 592);
+    SHARE_RUN(2, 16384, 1184);
+    SHARE_RUN(28, 8192, 148);
+  }
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
