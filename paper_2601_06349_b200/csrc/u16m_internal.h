@@ -25,7 +25,6 @@ cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t nu
                            uint16_t* out, cudaStream_t stream);
 
 constexpr int kDefaultInplaceGran = 2;
-constexpr int kDefaultStreamVecs = 8;
 int inplace_granularity();
 
 // Part of a job: part = 0 all tiles, 1 only the two edge tiles (the only

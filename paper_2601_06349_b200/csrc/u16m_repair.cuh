@@ -67,35 +67,6 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
                : "memory");
 }
 
-// Cache-policy variants for A/B runs (stream kernel): loads 0 = ld.global.cs
-// (evict-first), 1 = ld.global.nc.L1::no_allocate, 2 = ld.global (default
-// policy), 3 = ld.global.L2::256B (L2 sector prefetch); stores 0 =
-// st.global.cs, 1 = st.global (default policy).
-template <int kLd>
-__device__ __forceinline__ uint4 ld_hint(const uint4* p) {
-  uint4 v;
-  if constexpr (kLd == 1) {
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  } else if constexpr (kLd == 2) {
-    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  } else if constexpr (kLd == 3) {
-    asm volatile("ld.global.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  } else {
-    v = ld_stream(p);
-  }
-  return v;
-}
-template <int kSt>
-__device__ __forceinline__ void st_hint(uint4* p, uint4 v) {
-  if constexpr (kSt == 1) {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-  } else {
-    st_stream(p, v);
-  }
-}
-
 // High/low-surrogate flags for the 4 units in words (wa, wb): bit 7 of byte
 // lane j is set iff unit j is a high (H) / low (L) surrogate.
 __device__ __forceinline__ void classify4(uint32_t wa, uint32_t wb, uint32_t& H, uint32_t& L) {

@@ -33,9 +33,9 @@ constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;  // 2048 vectors = 32 K
 
 // kBE: units are big-endian in memory (fused byte-order handling, §8(f-3));
 // kCount: add the number of rewritten units to *count (CTA reduction, one
-// atomic per CTA); kNoStore: validation only; kHint: cache-policy A/B.
+// atomic per CTA); kNoStore: validation only.
 template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false,
-          int kHint = 0, bool kNoStore = false>
+          bool kNoStore = false>
 __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count) {
   constexpr int kSWarpVecs = 32 * kSV;
   constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   if (s.tile_sel == kTilesEdges) nwork = ntiles < 2 ? ntiles : 2;
   if (s.tile_sel == kTilesInterior) nwork = ntiles > 2 ? ntiles - 2 : 0;
   uint32_t counted = 0;
-  // One tile per CTA normally; a smaller (persistent) grid strides over tiles.
+  // One tile per CTA (persistent grids measured 15-20 % slower: profiles/README.md).
   for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
   uint64_t tile = w;
   if (s.tile_sel == kTilesEdges) tile = w == 0 ? 0 : ntiles - 1;
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   if (interior) {
     const uint4* src = s.in + v0;
 #pragma unroll
-    for (int k = 0; k < kSV; k++) v[k] = ld_hint<kHint / 4>(src + k * 32);
+    for (int k = 0; k < kSV; k++) v[k] = ld_stream(src + k * 32);
     const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
     if (lane == 0) halo = to_mem<kBE>(src16[-1]);
     if (lane == 31) halo = to_mem<kBE>(src16[(kSV - 1) * 32 * 8 + 8]);
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
 #pragma unroll
     for (int k = 0; k < kSV; k++) {
       const uint64_t vi = v0 + k * 32;
-      v[k] = vi < vend ? ld_hint<kHint / 4>(s.in + vi) : make_uint4(0, 0, 0, 0);
+      v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
     }
     // unit_at returns unit values for halos but raw memory words in range.
     const uint64_t warp_v0 = v0 - lane;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
     if (kNoStore) {
       // validation only (count)
     } else if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
-      if (store) st_hint<kHint % 4>(dst + k * 32, blend<kBE>(v[k], B0, B1));
+      if (store) st_stream(dst + k * 32, blend<kBE>(v[k], B0, B1));
     } else if (store && vi < vend) {
       const uint4 r = blend<kBE>(v[k], B0, B1);
 #pragma unroll
@@ -410,47 +410,12 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
 }
 
 
-// Vectors per thread of the stream kernel (U16M_STREAM_VECS: 8, 12 or 16;
-// A/B knob — register-staged bytes in flight per SM vs occupancy).
-static int stream_vecs() {
-  static const int v = [] {
-    const char* e = std::getenv("U16M_STREAM_VECS");
-    const int x = e ? std::atoi(e) : kDefaultStreamVecs;
-    return (x == 4 || x == 8 || x == 12 || x == 16) ? x : kDefaultStreamVecs;
-  }();
-  return v;
-}
-
 static int prefetch_setting() {
   static const int v = [] {
     const char* e = std::getenv("U16M_PREFETCH");
     return e ? std::atoi(e) : -1;  // -1: auto (one resident wave ahead)
   }();
   return v;
-}
-
-static int persist_setting() {  // U16M_PERSIST=N: grid of N CTAs per SM (A/B)
-  static const int v = [] {
-    const char* e = std::getenv("U16M_PERSIST");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
-static int hint_setting() {
-  static const int v = [] {
-    const char* l = std::getenv("U16M_LDHINT");
-    const char* t = std::getenv("U16M_STHINT");
-    const int ld = l ? std::atoi(l) : 0, st = t ? std::atoi(t) : 0;
-    return (ld >= 0 && ld < 4 ? ld : 0) * 4 + (st == 1 ? 1 : 0);
-  }();
-  return v;
-}
-
-template <int kHint>
-static void launch_hinted(const Span& s, unsigned g, cudaStream_t stream) {
-  if (s.in != s.out) stream_kernel<false, 1, 8, 4, false, false, kHint><<<g, kSThreads, 0, stream>>>(s, nullptr);
-  else stream_kernel<true, 2, 8, 4, false, false, kHint><<<g, kSThreads, 0, stream>>>(s, nullptr);
 }
 
 template <int kV, int kMB>
@@ -471,28 +436,7 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
     // (measured: +3% on config 1, a small loss on the 2-wave config 0).
     s.prefetch_tiles = pf >= 0 ? pf : (ntiles > static_cast<uint64_t>(2 * sms * kMB) ? sms * kMB : 0);
   }
-  if (persist_setting() > 0) {
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t cap = static_cast<uint64_t>(sms) * persist_setting();
-    if (grid > cap) grid = cap;
-    s.prefetch_tiles = 0;
-  }
   const unsigned g = static_cast<unsigned>(grid);
-  const int hint = hint_setting();
-  if (kV == 8 && hint != 0 && (s.in != s.out || inplace_granularity() == 2)) {
-    switch (hint) {
-      case 1: launch_hinted<1>(s, g, stream); break;
-      case 4: launch_hinted<4>(s, g, stream); break;
-      case 5: launch_hinted<5>(s, g, stream); break;
-      case 8: launch_hinted<8>(s, g, stream); break;
-      case 9: launch_hinted<9>(s, g, stream); break;
-      case 12: launch_hinted<12>(s, g, stream); break;
-      default: launch_hinted<13>(s, g, stream); break;
-    }
-    note_launch();
-    return cudaGetLastError();
-  }
   if (s.in != s.out) {
     stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr);
   } else {
@@ -550,7 +494,7 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
   s.tile_sel = kTilesAll;
   s.prefetch_tiles = 0;
   const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kSCtaVecs - 1) / kSCtaVecs;
-  stream_kernel<false, 1, 8, 4, false, true, 0, true><<<static_cast<unsigned>(ntiles), kSThreads, 0, stream>>>(s, count);
+  stream_kernel<false, 1, 8, 4, false, true, true><<<static_cast<unsigned>(ntiles), kSThreads, 0, stream>>>(s, count);
   note_launch();
   return cudaGetLastError();
 }
@@ -585,12 +529,7 @@ cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out,
 }
 
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream) {
-  switch (stream_vecs()) {
-    case 4: return launch_stream_v<4, 6>(s, part, stream);
-    case 12: return launch_stream_v<12, 3>(s, part, stream);
-    case 16: return launch_stream_v<16, 2>(s, part, stream);
-    default: return launch_stream_v<8, 4>(s, part, stream);
-  }
+  return launch_stream_v<kSV, 4>(s, part, stream);
 }
 
 }  // namespace u16m
