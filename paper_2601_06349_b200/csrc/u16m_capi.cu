@@ -86,7 +86,7 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // engines both stay busy (PCIe full duplex) while the kernel runs between
 // them.
 constexpr int kRing = 8;
-constexpr size_t kChunkUnits = size_t(32) << 20;  // ring buffer size: 64 MiB
+constexpr size_t kChunkUnits = size_t(32) << 20;  // largest chunk: 64 MiB
 
 // Pipeline chunk in units (U16M_PIPE_CHUNK_KIB overrides; at most kChunkUnits).
 size_t pipe_chunk_units() {
@@ -121,13 +121,25 @@ HostPipe* pipe_for(int device, u16m_status* st) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&p->counter, sizeof(unsigned long long));
   for (int i = 0; i < kRing && e == cudaSuccess; i++) {
-    e = cudaMalloc(&p->dbuf[i], kChunkUnits * sizeof(uint16_t));
+    e = cudaMalloc(&p->dbuf[i], pipe_chunk_units() * sizeof(uint16_t));  // 8 x 32 MiB by default
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->loaded[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->repaired[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->drained[i], cudaEventDisableTiming);
   }
   if (e != cudaSuccess) {
     *st = cuda_fail(e, "host pipeline setup");
+    for (int i = 0; i < kRing; i++) {  // release what was created (null handles are skipped)
+      if (p->dbuf[i]) cudaFree(p->dbuf[i]);
+      if (p->loaded[i]) cudaEventDestroy(p->loaded[i]);
+      if (p->repaired[i]) cudaEventDestroy(p->repaired[i]);
+      if (p->drained[i]) cudaEventDestroy(p->drained[i]);
+    }
+    if (p->counter) cudaFree(p->counter);
+    if (p->h2d) cudaStreamDestroy(p->h2d);
+    if (p->comp) cudaStreamDestroy(p->comp);
+    if (p->d2h) cudaStreamDestroy(p->d2h);
+    delete p;
+    cudaGetLastError();
     return nullptr;
   }
   g_pipes.push_back(p);

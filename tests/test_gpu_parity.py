@@ -169,6 +169,26 @@ def test_valid_pair_straddling_every_position(P, cuda):
         assert (gpu_inplace(P, x) == x).all()
 
 
+def test_every_unit_value_in_every_lane(P, cuda):
+    """The SWAR classification on the GPU for all 65 536 unit values
+    (proj/tests/test_surrogate.cpp:24-33 pins the predicates exhaustively):
+    each value u appears as [u, DC00] (pairs iff H(u)) and [D800, u] (pairs
+    iff L(u)), in 7-unit records so u visits every lane of a 16-byte vector."""
+    u = np.arange(1 << 16, dtype=np.uint16)
+    rec = np.empty((1 << 16, 7), np.uint16)
+    rec[:, 0], rec[:, 1], rec[:, 2] = u, 0xDC00, 0x41
+    rec[:, 3], rec[:, 4], rec[:, 5], rec[:, 6] = 0xD800, u, 0x41, 0x41
+    x = rec.reshape(-1)
+    e = O.fix_scalar(x)
+    assert (gpu_copy(P, x) == e).all()
+    assert (gpu_inplace(P, x) == e).all()
+    assert (O.stencil(x) == e).all()
+    # the 1-unit strings of the batched form see no neighbours at all
+    offs = np.arange(u.size + 1, dtype=np.int64)
+    z = P.to_well_formed_batched(dev(u), torch.from_numpy(offs).cuda())
+    assert (host(z) == np.where((u & 0xF800) == 0xD800, 0xFFFD, u)).all()
+
+
 def test_well_formed_in_place_identity(P, cuda):
     x = np.frombuffer(P.generate_utf16le(400_000, 0.05, 0.0, 77), np.uint16)
     assert P.is_well_formed_utf16le(x.tobytes())
