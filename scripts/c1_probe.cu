@@ -323,6 +323,61 @@ int main() {
     CK(cudaMalloc(&o, cb));
     float ms = timeit([&] { empty_kernel<<<1, 32>>>(); });
     printf("%-44s %8.1f us\n", "c0: empty kernel (event overhead)", ms * 1e3);
+    {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      float best = 1e9, sum = 0;
+      for (int r = 0; r < 20; r++) {  // no flush before the pair
+        cudaEventRecord(a);
+        empty_kernel<<<1, 32>>>();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float m;
+        cudaEventElapsedTime(&m, a, b);
+        best = std::min(best, m);
+        sum += m;
+      }
+      printf("%-44s %8.1f us (mean %.1f)\n", "empty kernel, no flush before", best * 1e3, sum / 20 * 1e3);
+      best = 1e9;
+      for (int r = 0; r < 20; r++) {  // flush, then a tiny kernel, then the pair
+        flush_kernel<<<148 * 8, 256>>>(g_flush, g_flush_n, g_sink);
+        empty_kernel<<<1, 32>>>();
+        cudaEventRecord(a);
+        empty_kernel<<<1, 32>>>();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float m;
+        cudaEventElapsedTime(&m, a, b);
+        best = std::min(best, m);
+      }
+      printf("%-44s %8.1f us\n", "empty kernel, flush + tiny kernel before", best * 1e3);
+      best = 1e9;
+      for (int r = 0; r < 20; r++) {  // flush, sync, then the pair
+        flush_kernel<<<148 * 8, 256>>>(g_flush, g_flush_n, g_sink);
+        cudaDeviceSynchronize();
+        cudaEventRecord(a);
+        empty_kernel<<<1, 32>>>();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float m;
+        cudaEventElapsedTime(&m, a, b);
+        best = std::min(best, m);
+      }
+      printf("%-44s %8.1f us\n", "empty kernel, flush + sync before", best * 1e3);
+      best = 1e9;
+      for (int r = 0; r < 20; r++) {  // flush, then pair around a 1184-CTA empty grid
+        flush_kernel<<<148 * 8, 256>>>(g_flush, g_flush_n, g_sink);
+        cudaEventRecord(a);
+        empty_kernel<<<148 * 8, 256>>>();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float m;
+        cudaEventElapsedTime(&m, a, b);
+        best = std::min(best, m);
+      }
+      printf("%-44s %8.1f us\n", "empty 1184x256 grid after flush", best * 1e3);
+    }
     ms = timeit([&] { cudaMemcpyAsync(o, d, cb, cudaMemcpyDeviceToDevice); });
     printf("%-44s %8.1f us  input %7.1f GB/s\n", "c0: cudaMemcpy D2D 32 MiB", ms * 1e3, cb / ms / 1e6);
     ms = timeit([&] { ldg_copy<8><<<cb / (16 * 256 * 8), 256>>>(d, o); });
