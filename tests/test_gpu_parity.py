@@ -226,6 +226,19 @@ def test_batched_edges(P, cuda):
     got = host(P.to_well_formed_batched(dev(data), torch.from_numpy(offsets).cuda()))
     assert (got == e).all()
     assert (got[:5] == data[:5]).all() and (got[offsets[-1]:] == data[offsets[-1]:]).all()
+    # strings covering only the middle of a large buffer: whole CTA tiles lie
+    # before offsets[0] and after offsets[S] and must be left untouched
+    data = rng.choice(ALPHABET, 300_001)
+    for lo, hi in ((50_001, 150_003), (16_384, 32_768), (0, 299_990), (299_000, 300_001)):
+        cuts = np.sort(rng.integers(lo, hi, 40))
+        offsets = np.concatenate([[lo], cuts, [hi]]).astype(np.int64)
+        e = O.fix_batched(data, offsets)
+        t = dev(data)
+        got = host(P.to_well_formed_batched(t, torch.from_numpy(offsets).cuda()))
+        assert (got == e).all(), (lo, hi)
+        assert (got[:lo] == data[:lo]).all() and (got[hi:] == data[hi:]).all()
+        P.to_well_formed_batched(t, torch.from_numpy(offsets).cuda(), out=t)
+        assert (host(t) == e).all(), (lo, hi, "in place")
 
 
 def test_batched_tile_records(P, cuda):
