@@ -50,7 +50,8 @@ cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out,
 // per-call workspaces stay cheap).
 void keep_pool_memory();
 // Count of units repair would rewrite, read-only stream kernel (adds to *count).
-cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream);
+cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream,
+                                uint32_t* half_tile_counts = nullptr);
 // Batched form with the buffer length known: tile table pre-pass + one tile
 // per CTA (u16m_stream.cu). offsets[S] <= n_units.
 bool batched_tiles_enabled();

@@ -27,6 +27,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
@@ -42,7 +43,7 @@ enum Mode : int {
   kCopy = 0,       // out = repair(in)
   kInPlace = 1,    // buf = repair(buf), stores only vectors with a rewrite
   // 2 was a count mode; counting now runs on the stream kernel (u16m_stream.cu)
-  kTileCount = 3,  // tile_counts[tile] = rewrites in that CTA tile
+  // 3 was a per-tile count mode; tile counts now come from the stream kernel
   kEmit = 4        // write ascending rewrite offsets (< limit) using tile prefixes
 };
 
@@ -54,8 +55,8 @@ struct BatchArgs {
 
 struct ScanArgs {
   unsigned long long* count_out;    // kEmit: number written
-  uint32_t* tile_counts;            // kTileCount output
   const unsigned long long* tile_prefix;  // kEmit input (exclusive prefix per tile)
+  const uint32_t* tile_counts;      // kEmit input (rewrites per tile)
   unsigned long long* offsets_out;  // kEmit output
   unsigned long long limit;         // kEmit cap
 };
@@ -119,7 +120,7 @@ __device__ __forceinline__ void tile_bad(const Flags (&f)[kVecs], uint32_t halo,
 
 template <int kMode, bool kSamePhase, bool kBatched, int kGran = 1>
 __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, ScanArgs sc) {
-  constexpr bool kScanMode = kMode == kTileCount || kMode == kEmit;
+  constexpr bool kScanMode = kMode == kEmit;
   __shared__ uint32_t starts[kBatched ? (kCtaUnits / 32 + 2) : 1];
   __shared__ unsigned long long warp_sums[kScanMode ? kWarps : 1];
   const int lane = threadIdx.x & 31;
@@ -147,15 +148,19 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
     tbase = 1;
   }
 
+  // kEmit: min(limit, total rewrites), written by tile_prefix_kernel; a tile
+  // whose prefix reaches it holds nothing to emit, nor does any later tile.
+  unsigned long long emit_stop = 0;
+  if constexpr (kMode == kEmit) emit_stop = *sc.count_out;
   for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
     const uint64_t tile = s.tile_sel == kTilesEdges && w == 1 ? ntiles - 1 : tbase + w;
     if constexpr (kMode == kEmit) {
-      // Tiles whose rewrites all rank past the limit contribute nothing: skip
-      // them before touching their data (the CLI asks for 10 offsets).
-      if (sc.tile_prefix[tile] >= sc.limit) {
-        if (tile + 1 == ntiles && threadIdx.x == 0) *sc.count_out = sc.limit;
-        continue;
-      }
+      // Tile prefixes are non-decreasing, so once a tile's rewrites all rank
+      // past the limit (or there are none left) the same holds for every later
+      // tile: stop before touching data (the CLI asks for 10 offsets; the grid
+      // is persistent).
+      if (sc.tile_prefix[tile] >= emit_stop) break;
+      if (sc.tile_counts[tile] == 0) continue;  // nothing to emit: skip the data
     }
     const uint64_t cta_v0 = vbeg + tile * kCtaVecs;
     const uint64_t warp_v0 = cta_v0 + static_cast<uint64_t>(warp) * kWarpVecs;
@@ -220,7 +225,7 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
     }
     uint32_t B0[kVecs], B1[kVecs];
     tile_bad<kBatched>(f, halo, lane, starts, (lane_off - lane) * 8, B0, B1);
-    if constexpr (kMode >= kTileCount) {
+    if constexpr (kMode == kEmit) {
 #pragma unroll
       for (int k = 0; k < kVecs; k++)
         if (edge[k]) mask_outside(s, warp_v0 + k * 32 + lane, B0[k], B1[k]);
@@ -268,33 +273,23 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
       __syncthreads();  // previous tile's readers of warp_sums are done
       if (lane == 0) warp_sums[warp] = warp_total;
       __syncthreads();
-      unsigned long long before = 0, tile_total = 0;
+      unsigned long long before = 0;
 #pragma unroll
-      for (int w = 0; w < kWarps; w++) {
+      for (int w = 0; w < kWarps; w++)
         if (w < warp) before += warp_sums[w];
-        tile_total += warp_sums[w];
-      }
-      if constexpr (kMode == kTileCount) {
-        if (threadIdx.x == 0) sc.tile_counts[tile] = static_cast<uint32_t>(tile_total);
-      } else {
-        const unsigned long long base = sc.tile_prefix[tile] + before;
-        if (base < sc.limit) {
+      const unsigned long long base = sc.tile_prefix[tile] + before;
+      if (base < sc.limit) {
 #pragma unroll
-          for (int k = 0; k < kVecs; k++) {
-            unsigned long long r = base + pre[k];
-            const uint64_t vi = warp_v0 + k * 32 + lane;
-            uint64_t bits = static_cast<uint64_t>(B0[k]) | (static_cast<uint64_t>(B1[k]) << 32);
-            while (bits && r < sc.limit) {
-              const int bit = __ffsll(static_cast<long long>(bits)) - 1;
-              bits &= bits - 1;
-              const uint64_t a = vi * 8 + (bit >> 3);
-              sc.offsets_out[r++] = a - s.lo;
-            }
+        for (int k = 0; k < kVecs; k++) {
+          unsigned long long r = base + pre[k];
+          const uint64_t vi = warp_v0 + k * 32 + lane;
+          uint64_t bits = static_cast<uint64_t>(B0[k]) | (static_cast<uint64_t>(B1[k]) << 32);
+          while (bits && r < sc.limit) {
+            const int bit = __ffsll(static_cast<long long>(bits)) - 1;
+            bits &= bits - 1;
+            const uint64_t a = vi * 8 + (bit >> 3);
+            sc.offsets_out[r++] = a - s.lo;
           }
-        }
-        if (tile + 1 == ntiles && threadIdx.x == 0) {
-          const unsigned long long all = sc.tile_prefix[tile] + tile_total;
-          *sc.count_out = all < sc.limit ? all : sc.limit;
         }
       }
     }
@@ -455,31 +450,72 @@ cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long lo
   return launch_stream_count(in, n, count_out, stream);
 }
 
-// Exclusive prefix over per-tile counts, one CTA, sequential chunks of 1024.
+// Exclusive prefix over per-tile counts in one CTA, 32768 tiles per round:
+// every thread loads its 32 consecutive counts with 8 independent 128-bit
+// loads (the whole round in flight at once), scans them in registers, and a
+// warp-shuffle + shared-memory block scan over the thread totals gives each
+// thread its offset; prefixes are written back as 128-bit stores. `counts`
+// and `prefix` are 16-byte aligned. Also writes *count_out = min(total,
+// limit), the number of offsets the emit pass writes.
+constexpr int kPrefixPer = 32;
 __global__ void __launch_bounds__(1024) tile_prefix_kernel(const uint32_t* counts, uint64_t n,
-                                                           unsigned long long* prefix) {
+                                                           unsigned long long* prefix, unsigned long long limit,
+                                                           unsigned long long* count_out) {
   __shared__ unsigned long long warp_tot[32];
-  __shared__ unsigned long long carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint64_t base = 0; base < n; base += 1024) {
-    const uint64_t i = base + threadIdx.x;
-    const unsigned long long c = i < n ? counts[i] : 0;
-    unsigned long long x = c;
+  unsigned long long carry = 0;
+  for (uint64_t base = 0; base < n; base += 1024 * kPrefixPer) {
+    const uint64_t i0 = base + static_cast<uint64_t>(threadIdx.x) * kPrefixPer;
+    uint32_t c[kPrefixPer];
+    if (i0 + kPrefixPer <= n) {
+      const uint4* src = reinterpret_cast<const uint4*>(counts + i0);
+#pragma unroll
+      for (int q = 0; q < kPrefixPer / 4; q++) {
+        const uint4 v = src[q];
+        c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPrefixPer; j++) c[j] = i0 + j < n ? counts[i0 + j] : 0u;
+    }
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int j = 0; j < kPrefixPer; j++) sum += c[j];
+    unsigned long long x = sum;  // inclusive scan of the thread sums within the warp
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long y = __shfl_up_sync(kFull, x, o);
       if (lane >= o) x += y;
     }
+    __syncthreads();  // previous round's readers of warp_tot are done
     if (lane == 31) warp_tot[warp] = x;
     __syncthreads();
-    unsigned long long before = carry;
-    for (int w = 0; w < warp; w++) before += warp_tot[w];
-    if (i < n) prefix[i] = before + x - c;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = before + x;
-    __syncthreads();
+    unsigned long long run = carry + x - sum, round_total = 0;
+    for (int w = 0; w < 32; w++) {
+      if (w < warp) run += warp_tot[w];
+      round_total += warp_tot[w];
+    }
+    if (i0 + kPrefixPer <= n) {
+      ulonglong2* dst = reinterpret_cast<ulonglong2*>(prefix + i0);
+#pragma unroll
+      for (int q = 0; q < kPrefixPer / 2; q++) {
+        ulonglong2 w2;
+        w2.x = run;
+        run += c[2 * q];
+        w2.y = run;
+        run += c[2 * q + 1];
+        dst[q] = w2;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPrefixPer; j++) {
+        if (i0 + j < n) prefix[i0 + j] = run;
+        run += c[j];
+      }
+    }
+    carry += round_total;
   }
+  if (threadIdx.x == 0) *count_out = carry < limit ? carry : limit;
 }
 
 cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
@@ -489,28 +525,34 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   if (e != cudaSuccess || n == 0 || limit == 0) return e;
   bool same = false;
   const Span s = make_span(in, n, nullptr, -1, -1, nullptr, nullptr, &same);
-  const uint64_t tiles = tiles_for(s);
+  const uint64_t tiles = tiles_for(s);  // 8192-unit tiles of the emit pass
+  const uint64_t halves = 2 * (((s.hi + 7) / 8 - s.lo / 8 + 2 * kCtaVecs - 1) / (2 * kCtaVecs));
   void* ws = nullptr;
   keep_pool_memory();
-  e = cudaMallocAsync(&ws, tiles * (sizeof(uint32_t) + sizeof(unsigned long long)) + 16, stream);
+  const size_t counts_bytes = (halves * sizeof(uint32_t) + 15) / 16 * 16;
+  e = cudaMallocAsync(&ws, counts_bytes + tiles * sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
-  auto* prefix = static_cast<unsigned long long*>(ws);
-  auto* counts = reinterpret_cast<uint32_t*>(prefix + tiles);
-  ScanArgs sc = kNoScan;
-  sc.tile_counts = counts;
-  e = launch<kTileCount, true, false>(s, kNoBatch, sc, tiles, stream);
+  auto* counts = static_cast<uint32_t*>(ws);  // both 16-byte aligned (tile_prefix_kernel)
+  auto* prefix = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + counts_bytes);
+  // 1) rewrites per 8192-unit tile: the read-only stream kernel (8 vectors in
+  //    flight per thread) writes one count per half of its 16384-unit tile;
+  // 2) exclusive prefix + the total; 3) emit on a persistent grid that stops
+  //    at the first tile ranked past the limit.
+  e = launch_stream_count(in, n, nullptr, stream, counts);
   if (e == cudaSuccess) {
-    tile_prefix_kernel<<<1, 1024, 0, stream>>>(counts, tiles, prefix);
+    tile_prefix_kernel<<<1, 1024, 0, stream>>>(counts, tiles, prefix, limit, count_out);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) {
-    sc = kNoScan;
+    ScanArgs sc = kNoScan;
     sc.count_out = count_out;
     sc.tile_prefix = prefix;
+    sc.tile_counts = counts;
     sc.offsets_out = offsets_out;
     sc.limit = limit;
-    e = launch<kEmit, true, false>(s, kNoBatch, sc, tiles, stream);
+    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count_for_current_device()) * 8);
+    e = launch<kEmit, true, false>(s, kNoBatch, sc, grid, stream);
   }
   const cudaError_t f = cudaFreeAsync(ws, stream);
   return e != cudaSuccess ? e : f;

@@ -36,7 +36,8 @@ constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;  // 2048 vectors = 32 K
 // atomic per CTA); kNoStore: validation only.
 template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false,
           bool kNoStore = false>
-__global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count) {
+__global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count,
+                                                                      uint32_t* half_tile_counts) {
   constexpr int kSWarpVecs = 32 * kSV;
   constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
   const int lane = threadIdx.x & 31;
@@ -154,10 +155,23 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
     if (lane == 0) warp_counts[threadIdx.x / 32] = counted;
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long c = 0;
+      if (half_tile_counts) {
+        // Per 8192-unit half tile (warps 0-3 / 4-7): the tile counts of the
+        // offsets scan, in the general kernel's tile geometry (u16m_kernels.cu).
+        uint32_t c0 = 0, c1 = 0;
 #pragma unroll
-      for (int w = 0; w < kSThreads / 32; w++) c += warp_counts[w];
-      if (c) atomicAdd(count, c);
+        for (int w = 0; w < kSThreads / 64; w++) {
+          c0 += warp_counts[w];
+          c1 += warp_counts[w + kSThreads / 64];
+        }
+        half_tile_counts[2 * blockIdx.x] = c0;
+        half_tile_counts[2 * blockIdx.x + 1] = c1;
+      } else {
+        unsigned long long c = 0;
+#pragma unroll
+        for (int w = 0; w < kSThreads / 32; w++) c += warp_counts[w];
+        if (c) atomicAdd(count, c);
+      }
     }
   }
 }
@@ -438,13 +452,13 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
   }
   const unsigned g = static_cast<unsigned>(grid);
   if (s.in != s.out) {
-    stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr);
+    stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr);
   } else {
     switch (inplace_granularity()) {
-      case 1: stream_kernel<true, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr); break;
-      case 4: stream_kernel<true, 4, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr); break;
-      case 8: stream_kernel<true, 8, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr); break;
-      default: stream_kernel<true, 2, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr); break;
+      case 1: stream_kernel<true, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr); break;
+      case 4: stream_kernel<true, 4, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr); break;
+      case 8: stream_kernel<true, 8, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr); break;
+      default: stream_kernel<true, 2, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr); break;
     }
   }
   note_launch();
@@ -455,9 +469,9 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
 template <bool kInPlace, bool kBE>
 static void launch_codec_t(const Span& s, unsigned g, unsigned long long* count, cudaStream_t stream) {
   if (count)
-    stream_kernel<kInPlace, 2, 8, 4, kBE, true><<<g, kSThreads, 0, stream>>>(s, count);
+    stream_kernel<kInPlace, 2, 8, 4, kBE, true><<<g, kSThreads, 0, stream>>>(s, count, nullptr);
   else
-    stream_kernel<kInPlace, 2, 8, 4, kBE, false><<<g, kSThreads, 0, stream>>>(s, nullptr);
+    stream_kernel<kInPlace, 2, 8, 4, kBE, false><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr);
 }
 
 cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long long* count, cudaStream_t stream) {
@@ -478,8 +492,11 @@ cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long lo
 }
 
 // Validation (§8(f-1)): the stream kernel with the count and no stores —
-// 2 B/unit read-only, one tile per CTA.
-cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream) {
+// 2 B/unit read-only, one tile per CTA. With half_tile_counts set it writes
+// the rewrite count of every 8192-unit half tile instead of the total
+// (2 * ceil(n_vectors / 2048) entries).
+cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream,
+                                uint32_t* half_tile_counts) {
   if (n == 0) return cudaSuccess;
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
@@ -494,7 +511,8 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
   s.tile_sel = kTilesAll;
   s.prefetch_tiles = 0;
   const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kSCtaVecs - 1) / kSCtaVecs;
-  stream_kernel<false, 1, 8, 4, false, true, true><<<static_cast<unsigned>(ntiles), kSThreads, 0, stream>>>(s, count);
+  stream_kernel<false, 1, 8, 4, false, true, true>
+      <<<static_cast<unsigned>(ntiles), kSThreads, 0, stream>>>(s, count, half_tile_counts);
   note_launch();
   return cudaGetLastError();
 }

@@ -15,10 +15,16 @@ x = _lib.gen_config(1, n, seed=1)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
 offs = torch.zeros(10, dtype=torch.int64, device="cuda")
+alloffs = torch.zeros(n // 16, dtype=torch.int64, device="cuda")
+clean = _lib.to_well_formed(x)  # well-formed input: nothing to report
 s = torch.cuda.current_stream().cuda_stream
 for name, fn in (("count_unpaired", lambda: L.u16m_count_unpaired(x.data_ptr(), n, cnt.data_ptr(), s)),
                  ("unpaired_offsets(limit=10)",
-                  lambda: L.u16m_unpaired_offsets(x.data_ptr(), n, 10, offs.data_ptr(), cnt.data_ptr(), s))):
+                  lambda: L.u16m_unpaired_offsets(x.data_ptr(), n, 10, offs.data_ptr(), cnt.data_ptr(), s)),
+                 ("unpaired_offsets(limit=10), well-formed input",
+                  lambda: L.u16m_unpaired_offsets(clean.data_ptr(), n, 10, offs.data_ptr(), cnt.data_ptr(), s)),
+                 ("unpaired_offsets(all, 8.3M offsets)",
+                  lambda: L.u16m_unpaired_offsets(x.data_ptr(), n, n // 16, alloffs.data_ptr(), cnt.data_ptr(), s))):
     tot = 0.0
     for i in range(13):
         _lib.l2_flush(flush)

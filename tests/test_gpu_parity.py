@@ -208,6 +208,26 @@ def test_count_and_offsets(P, cuda):
     assert P.unpaired_surrogate_offsets(O.u16([0x41, 0xDC00, 0x42, 0xD800]).tobytes(), 1) == [1]
 
 
+def test_offsets_many_tiles(P, cuda):
+    """unpaired offsets over more than one round of the single-CTA tile prefix
+    (32768 tiles of 8192 units): lone surrogates planted at known places in an
+    otherwise ASCII 2^28+ unit buffer, including the first and last unit."""
+    n = (1 << 28) + 12_345
+    rng = np.random.default_rng(5)
+    pos = np.unique(np.concatenate([[0, n - 1, 8191, 8192, (1 << 28) - 1, 1 << 28],
+                                    rng.integers(0, n, 5000)]))
+    pos = pos[np.concatenate([[True], np.diff(pos) > 1])]   # no two adjacent: each stays lone
+    t = torch.full((n,), 0x41, dtype=torch.int16, device="cuda")
+    idx = torch.from_numpy(pos.astype(np.int64)).cuda()
+    t[idx] = torch.tensor(np.where(pos % 2 == 0, 0xD800, 0xDC00).astype(np.uint16).view(np.int16)).cuda()
+    assert P.count_unpaired(t) == pos.size
+    assert P.unpaired_offsets_device(t).cpu().numpy().tolist() == pos.tolist()
+    for lim in (1, 10, 4999):
+        assert P.unpaired_offsets_device(t, lim).cpu().numpy().tolist() == pos[:lim].tolist()
+    clean = torch.full((n,), 0x41, dtype=torch.int16, device="cuda")
+    assert P.unpaired_offsets_device(clean, 10).numel() == 0
+
+
 def test_batched_edges(P, cuda):
     rng = np.random.default_rng(21)
     # string-edge semantics: H|L across an edge must both become FFFD
