@@ -509,8 +509,13 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
   s.left = s.right = -1;
   s.left_ptr = s.right_ptr = nullptr;
   s.tile_sel = kTilesAll;
-  s.prefetch_tiles = 0;
   const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kSCtaVecs - 1) / kSCtaVecs;
+  {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int pf = prefetch_setting();
+    s.prefetch_tiles = pf >= 0 ? pf : (ntiles > static_cast<uint64_t>(2 * sms * 4) ? sms * 4 : 0);
+  }
   stream_kernel<false, 1, 8, 4, false, true, true>
       <<<static_cast<unsigned>(ntiles), kSThreads, 0, stream>>>(s, count, half_tile_counts);
   note_launch();
