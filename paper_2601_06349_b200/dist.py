@@ -172,18 +172,48 @@ class PeerHalo:
         rebuild, args = reduce_tensor(shard)
         metas = [None] * world
         dist.all_gather_object(metas, (args, int(shard.numel())), group=group)
-        for r in range(self.rank - 1, -1, -1):
-            if metas[r][1] > 0:
-                t = rebuild(*metas[r][0])
-                self._peers.append(t)
-                self.left_ptr = t.data_ptr() + 2 * (t.numel() - 1)
-                break
-        for r in range(self.rank + 1, world):
-            if metas[r][1] > 0:
-                t = rebuild(*metas[r][0])
-                self._peers.append(t)
-                self.right_ptr = t.data_ptr()
-                break
+        me = shard.device.index
+
+        def open_on_my_device(a):
+            # reduce_tensor's args[6] is the producer's device index, and torch
+            # opens the IPC handle under that device, i.e. in the neighbour
+            # GPU's context of this process, where this rank's kernels could
+            # not dereference it. Opening it under THIS rank's device maps the
+            # neighbour's memory into our own context (cudaIpcOpenMemHandle
+            # with cudaIpcMemLazyEnablePeerAccess turns on NVLink peer access).
+            a = list(a)
+            owner = int(a[6])
+            if owner != me and not torch.cuda.can_device_access_peer(me, owner):
+                raise RuntimeError(f"cuda:{me} has no peer access to cuda:{owner}")
+            a[6] = me
+            return rebuild(*a)
+
+        err = None
+        try:
+            for r in range(self.rank - 1, -1, -1):
+                if metas[r][1] > 0:
+                    t = open_on_my_device(metas[r][0])
+                    self._peers.append(t)
+                    self.left_ptr = t.data_ptr() + 2 * (t.numel() - 1)
+                    break
+            for r in range(self.rank + 1, world):
+                if metas[r][1] > 0:
+                    t = open_on_my_device(metas[r][0])
+                    self._peers.append(t)
+                    self.right_ptr = t.data_ptr()
+                    break
+        except Exception as e:  # noqa: BLE001 - reported on every rank below
+            err = f"rank {self.rank}: {e!r}"
+        # Agree before anyone proceeds: if one rank cannot map its neighbours,
+        # every rank raises (callers fall back to the NCCL form together
+        # instead of deadlocking in a barrier).
+        errs = [None] * world
+        dist.all_gather_object(errs, err, group=group)
+        bad = [e for e in errs if e]
+        if bad:
+            self._peers.clear()
+            self.left_ptr = self.right_ptr = 0
+            raise RuntimeError("PeerHalo setup failed: " + "; ".join(bad))
         torch.cuda.synchronize(shard.device)
         dist.barrier(group=group)
 
