@@ -315,6 +315,12 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   for (int k = 0; k < kSV; k++) F |= static_cast<uint32_t>((M >> (8 * k)) & 1u) << k;
   const uint32_t Fd = __shfl_sync(kFull, F, (lane + 1) & 31);
   const uint32_t after = lane == 31 ? ((Fd >> 1) | (start_after ? (1u << (kSV - 1)) : 0u)) : Fd;
+  // Vectors k of this warp that hold a string start (or precede one): one
+  // warp reduction up front instead of a vote per vector.
+  uint32_t need = after;
+#pragma unroll
+  for (int k = 0; k < kSV; k++) need |= (static_cast<uint32_t>(M >> (8 * k)) & 0xFFu) ? (1u << k) : 0u;
+  need = __reduce_or_sync(kFull, need);
 
   Flags cur = classify8(v[0]);
   uint32_t hp_carry = hflag_hi(halo);
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
     const uint32_t aft = (after >> k) & 1u;
     // Most vectors of a warp hold no string start: skip the start-flag
     // algebra when no lane needs it (warp-uniform branch).
-    if (__any_sync(kFull, (bits | aft) != 0))
+    if ((need >> k) & 1u)
       bad8(cur, hp, ln, B0, B1, spread4(bits), spread4(bits >> 4), aft << 7);
     else
       bad8(cur, hp, ln, B0, B1);
