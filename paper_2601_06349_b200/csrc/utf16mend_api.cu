@@ -164,6 +164,12 @@ void to_well_formed_batched(std::span<const char16_t> in, std::span<const std::i
   copy(o, d.p, in.size_bytes(), cudaMemcpyDeviceToHost);
 }
 
+void fix_scalar(std::span<const char16_t> in, std::span<char16_t> out) { to_well_formed(in, out); }
+
+void fix_scalar(char16_t* out, const char16_t* in, std::size_t n) {
+  to_well_formed(std::span<const char16_t>(in, n), std::span<char16_t>(out, n));
+}
+
 bool is_well_formed(std::span<const char16_t> in) {
   if (in.empty()) return true;
   const auto* i = reinterpret_cast<const uint16_t*>(in.data());

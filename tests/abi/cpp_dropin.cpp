@@ -11,6 +11,14 @@
 #include <vector>
 
 #include "utf16mend/driver.hpp"
+#include "utf16mend/surrogate.hpp"
+
+// The per-unit predicates are constexpr, as the reference's call sites use
+// them (proj/tests/test_surrogate.cpp:11-48).
+static_assert(utf16mend::is_high_surrogate(0xDBFF) && !utf16mend::is_high_surrogate(0xDC00));
+static_assert(utf16mend::is_low_surrogate(0xDC00) && utf16mend::is_surrogate(0xDFFF));
+static_assert(utf16mend::classify(0x41) == utf16mend::surrogate_class::non_surrogate);
+static_assert(utf16mend::compose_code_point(0xD83D, 0xDE0A) == 0x1F60A);
 
 int main() {
   using namespace utf16mend;
@@ -35,6 +43,14 @@ int main() {
     std::vector<char16_t> buf = in;
     to_well_formed_in_place(buf, parse_kernel_id("generic8"));
     if (out != expected || buf != expected) return 1;
+    // surrogate.hpp entry points (reference out, in, n order; exact aliasing allowed)
+    std::vector<char16_t> fs(in.size()), alias = in;
+    fix_scalar(fs.data(), in.data(), in.size());
+    fix_scalar(std::span<const char16_t>(alias), std::span<char16_t>(alias));
+    if (fs != expected || alias != expected) return 1;
+    if (is_well_formed(in) || !is_well_formed(expected)) return 1;
+    if (unpaired_surrogate_offsets(in) != std::vector<std::size_t>{10, 21}) return 1;
+    if (unpaired_surrogate_offsets(in, 1) != std::vector<std::size_t>{10}) return 1;
     std::printf("repaired %s\n", to_string(select_kernel()).c_str());
     return 0;
   } catch (const std::runtime_error& e) {

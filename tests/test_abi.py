@@ -40,7 +40,9 @@ def test_cpp_api_symbols_exported():
     for sym in ("utf16mend::to_well_formed(", "utf16mend::to_well_formed_in_place(",
                 "utf16mend::to_well_formed_batched(", "utf16mend::parse_kernel_id(",
                 "utf16mend::select_kernel(", "utf16mend::available_kernels(",
-                "utf16mend::is_well_formed(", "utf16mend::unpaired_surrogate_offsets("):
+                "utf16mend::is_well_formed(", "utf16mend::unpaired_surrogate_offsets(",
+                "utf16mend::fix_scalar(char16_t*, char16_t const*, unsigned long)",
+                "utf16mend::fix_scalar(std::span<char16_t const"):
         assert sym in out, sym
 
 
