@@ -382,7 +382,10 @@ def run_ours(args):
     all_launches = P.launch_count() - launches0
 
     # correctness spot check of the last step against the first repair (cheap, device-side)
-    ok = P.count_unpaired(out) == 0 if mode != "batched" else True
+    # (batched: every repaired string is well-formed and none ends with a high
+    # or starts with a low surrogate, so the concatenation — config 3's whole
+    # buffer — is well-formed too)
+    ok = P.count_unpaired(out) == 0
 
     in_bytes = 2 * units
     extra = 8 * offsets.numel() if offsets is not None else 0
@@ -485,6 +488,7 @@ def run_ours(args):
                      "dram_frac_from_traffic": (round(traffic_for(args.config) / kernel_s / 1e9 / peak, 4)
                                                 if traffic_for(args.config) and world == 1 else None),
                      "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
+                     **({"frac_without_offsets": round(4 * units / kernel_s / 1e9 / peak, 4)} if extra else {}),
                      "kernel_ms": round(kernel_s * 1e3, 4)},
         "cpu_baseline": cpu,
         "e2e": e2e,
