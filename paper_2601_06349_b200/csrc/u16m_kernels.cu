@@ -362,8 +362,10 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // Kernel family selection. Default ("auto"): copy / in-place run the rolling
 // register-pipeline stream kernel (u16m_stream.cu; measured best: 6.9 TB/s
-// copy, config 1 in 133 us), the batched form runs the TMA-pipelined kernel
-// (its producer warp walks the offsets off the consumers' critical path).
+// copy, config 1 in 131 us); the length-aware batched entry runs the batched
+// tile kernel (u16m_stream.cu) and the length-less one the TMA-pipelined
+// kernel (its producer warp walks the offsets off the consumers' critical
+// path; a persistent grid needs no length).
 // U16M_KERNEL overrides for A/B runs (profiles/README.md has the numbers):
 // "tma" (TMA-pipelined for everything), "ldg" (register-staged everywhere;
 // the length-less batched entry then uses the general kernel), "general"
