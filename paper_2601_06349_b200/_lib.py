@@ -107,7 +107,14 @@ def raw():
 
 
 # ---- device tensor API -------------------------------------------------------
-def _units(t: torch.Tensor, name: str) -> torch.Tensor:
+def _units(t, name: str) -> torch.Tensor:
+    """Validate a device buffer of code units. Any DLPack producer (CuPy,
+    JAX, NumPy-on-device libraries, ...) is accepted zero-copy through
+    torch.from_dlpack; the returned tensor aliases its memory."""
+    if not isinstance(t, torch.Tensor) and hasattr(t, "__dlpack__"):
+        t = torch.from_dlpack(t)
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a CUDA tensor or a DLPack-exporting device array")
     if t.dtype not in (torch.int16, torch.uint16):
         raise ValueError(f"{name} must be an int16/uint16 tensor of UTF-16 code units")
     if not t.is_cuda:
@@ -125,10 +132,10 @@ def _stream(t: torch.Tensor, stream) -> int:
 
 def to_well_formed(x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """out = repair(x) on the GPU (reference to_well_formed, driver.hpp:64-65)."""
-    _units(x, "x")
+    x = _units(x, "x")
     if out is None:
         out = torch.empty_like(x)
-    _units(out, "out")
+    out = _units(out, "out")
     if out.numel() != x.numel():
         raise ValueError("to_well_formed: input and output lengths differ")
     with torch.cuda.device(x.device):
@@ -138,7 +145,7 @@ def to_well_formed(x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=N
 
 def to_well_formed_(x: torch.Tensor, stream=None) -> torch.Tensor:
     """In-place repair (reference to_well_formed_in_place, driver.hpp:68-69)."""
-    _units(x, "x")
+    x = _units(x, "x")
     with torch.cuda.device(x.device):
         _check(_L.u16m_to_well_formed_in_place(x.data_ptr(), x.numel(), _stream(x, stream)))
     return x
@@ -148,7 +155,7 @@ def to_well_formed_halo(x: torch.Tensor, out: Optional[torch.Tensor], left: int,
                         stream=None) -> torch.Tensor:
     """Repair one contiguous shard of a larger logical buffer; left/right are the
     neighbouring units (-1 at the logical buffer's ends). out=None: in place."""
-    _units(x, "x")
+    x = _units(x, "x")
     out = x if out is None else _units(out, "out")
     with torch.cuda.device(x.device):
         _check(_L.u16m_to_well_formed_halo(x.data_ptr(), x.numel(), out.data_ptr(), int(left), int(right),
@@ -163,7 +170,7 @@ def to_well_formed_part(x: torch.Tensor, out: Optional[torch.Tensor], part: int,
                         right_ptr: int = 0, stream=None) -> torch.Tensor:
     """One part (PART_EDGES / PART_INTERIOR / PART_ALL) of a shard repair; halo
     units are read on the device from left_ptr / right_ptr (0 = buffer end)."""
-    _units(x, "x")
+    x = _units(x, "x")
     out = x if out is None else _units(out, "out")
     with torch.cuda.device(x.device):
         _check(_L.u16m_to_well_formed_part(x.data_ptr(), x.numel(), out.data_ptr(), left_ptr or None,
@@ -174,14 +181,16 @@ def to_well_formed_part(x: torch.Tensor, out: Optional[torch.Tensor], part: int,
 def to_well_formed_batched(data: torch.Tensor, offsets: torch.Tensor, out: Optional[torch.Tensor] = None,
                            stream=None) -> torch.Tensor:
     """Repair every string [offsets[s], offsets[s+1]) independently."""
-    _units(data, "data")
+    data = _units(data, "data")
+    if not isinstance(offsets, torch.Tensor) and hasattr(offsets, "__dlpack__"):
+        offsets = torch.from_dlpack(offsets)
     if offsets.dtype != torch.int64 or not offsets.is_cuda or not offsets.is_contiguous():
         raise ValueError("offsets must be a contiguous int64 CUDA tensor")
     if offsets.numel() < 1:
         raise ValueError("offsets must have num_strings + 1 entries")
     if out is None:
         out = data.clone()
-    _units(out, "out")
+    out = _units(out, "out")
     if out.numel() != data.numel():
         raise ValueError("to_well_formed_batched: input and output lengths differ")
     with torch.cuda.device(data.device):
@@ -211,7 +220,7 @@ def to_well_formed_sharded(shards: Sequence[torch.Tensor], outs: Optional[Sequen
 
 def count_unpaired(x: torch.Tensor, stream=None) -> int:
     """Number of units repair would rewrite (0 <=> well-formed). Synchronises."""
-    _units(x, "x")
+    x = _units(x, "x")
     cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
     with torch.cuda.device(x.device):
         _check(_L.u16m_count_unpaired(x.data_ptr(), x.numel(), cnt.data_ptr(), _stream(x, stream)))
@@ -220,7 +229,7 @@ def count_unpaired(x: torch.Tensor, stream=None) -> int:
 
 def unpaired_offsets_device(x: torch.Tensor, limit: Optional[int] = None, stream=None) -> torch.Tensor:
     """Ascending offsets (int64 CUDA tensor) of the units repair would rewrite."""
-    _units(x, "x")
+    x = _units(x, "x")
     cap = x.numel() if limit is None else max(0, min(int(limit), x.numel()))
     offs = torch.empty(max(cap, 1), dtype=torch.int64, device=x.device)
     cnt = torch.zeros(1, dtype=torch.int64, device=x.device)
@@ -330,7 +339,7 @@ def to_well_formed_bytes(x: torch.Tensor, out: Optional[torch.Tensor] = None, bi
                          count: bool = False, stream=None):
     """Device form of fix_utf16_bytes: x holds units as raw int16 words in the
     given byte order. Returns out, or (out, replacements) when count=True."""
-    _units(x, "x")
+    x = _units(x, "x")
     out = torch.empty_like(x) if out is None else _units(out, "out")
     cnt = torch.zeros(1, dtype=torch.int64, device=x.device) if count else None
     with torch.cuda.device(x.device):

@@ -571,3 +571,32 @@ def test_batched_runs_of_empty_strings(P, cuda):
         u = t.clone()
         P.to_well_formed_batched(u, o, out=u)
         assert (host(u) == e).all(), ("in place", run)
+
+
+class _DLPackArray:
+    """A minimal foreign device array: only the DLPack protocol (as CuPy or
+    JAX arrays expose it)."""
+
+    def __init__(self, t):
+        self._t = t
+
+    def __dlpack__(self, **kw):
+        return self._t.__dlpack__(**kw)
+
+    def __dlpack_device__(self):
+        return self._t.__dlpack_device__()
+
+
+def test_dlpack_producers_zero_copy(P, cuda):
+    x = O.u16([0x41, 0xD800, 0x42, 0xDC00, 0xD83D, 0xDE0A, 0xDBFF])
+    e = O.fix_scalar(x)
+    t = dev(x)
+    assert (host(P.to_well_formed(_DLPackArray(t))) == e).all()
+    P.to_well_formed_(_DLPackArray(t))                     # repairs the producer's memory
+    assert (host(t) == e).all()
+    t = dev(x)
+    assert P.count_unpaired(_DLPackArray(t)) == 3
+    assert P.unpaired_offsets_device(_DLPackArray(t)).cpu().tolist() == [1, 3, 6]
+    offs = torch.tensor([0, 2, 7], dtype=torch.int64, device="cuda")
+    got = P.to_well_formed_batched(_DLPackArray(t), _DLPackArray(offs))
+    assert (host(got) == O.fix_batched(x, np.array([0, 2, 7]))).all()
