@@ -147,7 +147,10 @@ HostPipe* pipe_for(int device, u16m_status* st) {
 }
 
 // Host-path mode (U16M_HOST_MODE). Measured on the B200 box (scripts/
-// e2e_probe.py, 512 MiB, input GB/s, in place / copy):
+// e2e_probe.py, 512 MiB, input GB/s, in place / copy; the in-place input was
+// restored by a CPU memcpy right before each call, which alone costs the H2D
+// DMA ~15 %: 45.5-46.3 in place when it is restored by DMA instead,
+// scripts/e2e_timeline_probe.py; full-duplex PCIe tops out at 46-50 each way):
 //   staged (default): H2D copy -> kernel -> D2H copy, 3 streams   39.6-41.9 / 42-46
 //   writeback: in-place jobs on pinned mapped memory stage H2D by copy engine
 //              and the kernel stores only rewritten 32-byte groups straight
@@ -157,8 +160,8 @@ HostPipe* pipe_for(int device, u16m_status* st) {
 // the copy-engine pipeline stays the default. Also measured and dropped:
 // write-back at 64/128/256/512-byte groups (40.8/36.7/37.0/36.9 in place),
 // chunks of 4/8/12/16/24/64 MiB (34-40 in place; ~20 us fixed cost per
-// chunk), and a geometric ramp of the end chunks (no change: fill and drain
-// are not the loss).
+// chunk), and a geometric ramp of the end chunks (no change, re-measured with
+// the DMA-restored input: 46.0-46.3 with and without).
 enum HostMode { kHostStaged = 0, kHostWriteback = 1, kHostZeroCopy = 2 };
 int host_mode() {
   static const int m = [] {
