@@ -67,6 +67,14 @@ def main():
     assert (outp.numpy().view(np.uint16) == O.stencil(y)).all(), "host copy"
     assert L.u16m_to_well_formed_host(pin.data_ptr(), y.size, pin.data_ptr()) == 0
     assert (pin.numpy().view(np.uint16) == O.stencil(y)).all(), "host in place"
+    # pageable buffers (the CopyPool bounce-buffer path; with U16M_PIPE_CHUNK_KIB=64
+    # this is 10 chunks, more than the 4 pinned bounce buffers)
+    pg = y.view(np.int16).copy()
+    pgo = np.empty_like(pg)
+    assert L.u16m_to_well_formed_host(pg.ctypes.data, y.size, pgo.ctypes.data) == 0
+    assert (pgo.view(np.uint16) == O.stencil(y)).all(), "host pageable copy"
+    assert L.u16m_to_well_formed_host(pg.ctypes.data, y.size, pg.ctypes.data) == 0
+    assert (pg.view(np.uint16) == O.stencil(y)).all(), "host pageable in place"
     be, c = P.fix_utf16_bytes(y.astype(">u2").tobytes(), "be")
     assert np.frombuffer(be, ">u2").astype(np.uint16).tobytes() == O.stencil(y).tobytes(), "host codec"
     torch.cuda.synchronize()

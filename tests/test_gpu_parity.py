@@ -324,6 +324,16 @@ def test_host_pipeline_chunks(P, cuda):
     assert (outp.numpy().view(np.uint16) == e).all()
     assert L.u16m_to_well_formed_host(pin.data_ptr(), n, pin.data_ptr()) == 0
     assert (pin.numpy().view(np.uint16) == e).all()
+    # pageable memory, more chunks than pinned bounce buffers (5.3 x 32 MiB)
+    m = (16 << 20) * 5 + 4321
+    y = O.gen_config(1, m, seed=78)
+    ey = O.stencil_mt(y)
+    pg = y.view(np.int16).copy()
+    pgo = np.empty_like(pg)
+    assert L.u16m_to_well_formed_host(pg.ctypes.data, m, pgo.ctypes.data) == 0
+    assert (pgo.view(np.uint16) == ey).all()
+    assert L.u16m_to_well_formed_host(pg.ctypes.data, m, pg.ctypes.data) == 0
+    assert (pg.view(np.uint16) == ey).all()
 
 
 def test_sharded_virtual(P, cuda):
