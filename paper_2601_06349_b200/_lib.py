@@ -252,14 +252,6 @@ def _check_bytes(data) -> memoryview:
     return mv
 
 
-def _device_units(data) -> torch.Tensor:
-    mv = _check_bytes(data)
-    if mv.nbytes == 0:
-        return torch.empty(0, dtype=torch.int16, device="cuda")
-    host = torch.frombuffer(bytearray(mv), dtype=torch.int16)
-    return host.to("cuda", non_blocking=False)
-
-
 def fix_utf16le(data, kernel: Optional[str] = None) -> bytes:
     """Return `data` (raw UTF-16LE code units) with every unpaired surrogate
     replaced by U+FFFD (module.cpp:54-64). Host memory is staged through the
@@ -284,10 +276,29 @@ def fix_str(text: str, kernel: Optional[str] = None) -> str:
     return fix_utf16le(data, kernel).decode("utf-16-le")
 
 
+def _host_offsets(data, limit: int) -> list[int]:
+    """Chunked host-memory scan through the C ABI (u16m_unpaired_offsets_host):
+    the bytes are read in place (no Python-side copy) and streamed to the GPU;
+    the scan stops once `limit` offsets are found."""
+    import numpy as np
+
+    mv = _check_bytes(data)
+    n = mv.nbytes // 2
+    if n == 0 or limit <= 0:
+        return []
+    cap = min(int(limit), n)
+    src = np.frombuffer(mv, dtype=np.uint8)
+    if src.ctypes.data % 2:                     # the C ABI needs whole-unit alignment
+        src = src.copy()
+    out = np.empty(cap, dtype=np.uint64)
+    cnt = ctypes.c_size_t(0)
+    _check(_L.u16m_unpaired_offsets_host(src.ctypes.data, n, cap, out.ctypes.data, ctypes.byref(cnt)))
+    return [int(v) for v in out[: cnt.value]]
+
+
 def is_well_formed_utf16le(data) -> bool:
     """True if `data` contains no unpaired surrogate (module.cpp:66-70)."""
-    t = _device_units(data)
-    return t.numel() == 0 or count_unpaired(t) == 0
+    return not _host_offsets(data, 1)
 
 
 def is_well_formed_str(text: str) -> bool:
@@ -296,10 +307,7 @@ def is_well_formed_str(text: str) -> bool:
 
 def unpaired_surrogate_offsets(data, limit: int = 2**64 - 1) -> list[int]:
     """Unit offsets that fixing would rewrite, capped at `limit` (module.cpp:72-78)."""
-    t = _device_units(data)
-    if t.numel() == 0 or limit == 0:
-        return []
-    return [int(v) for v in unpaired_offsets_device(t, min(limit, t.numel())).cpu().tolist()]
+    return _host_offsets(data, limit)
 
 
 def generate_utf16le(units: int, pair_pct: float = 0.0, mismatch_pct: float = 0.0, seed: int = 0) -> bytes:

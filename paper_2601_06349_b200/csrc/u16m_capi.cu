@@ -650,23 +650,84 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
   *count_out = 0;
   if (n == 0 || limit == 0) return U16M_OK;
   if (in == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "null buffer with n > 0");
+  if (reinterpret_cast<uintptr_t>(in) & 1u) return fail(U16M_ERR_MISALIGNED, "in not 2-byte aligned");
   U16M_TRY(check_device_present());
   if (limit > n) limit = n;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(g_pipe_mu);
+  u16m_status st = U16M_OK;
+  HostPipe* p = pipe_for(dev, &st);
+  if (p == nullptr) return st;
+  // Chunked, read-only scan: chunk c+1 moves H2D (straight from pinned memory,
+  // or through a pinned bounce buffer filled by the CopyPool) while chunk c
+  // is scanned with its neighbours' units as halos; the scan stops at the
+  // first chunk that completes `limit` offsets (the CLI check asks for 10,
+  // is_well_formed for 1), so an ill-formed buffer is rarely read to its end.
+  const bool pinned = is_pinned(in);
+  const size_t chunk = pipe_chunk_units();
+  if (!pinned) {
+    for (int i = 0; i < 2; i++) {
+      if (p->stage[i]) continue;
+      e = cudaHostAlloc(reinterpret_cast<void**>(&p->stage[i]), chunk * sizeof(uint16_t), cudaHostAllocDefault);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->staged[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) {
+        if (p->stage[i]) cudaFreeHost(p->stage[i]);
+        p->stage[i] = nullptr;
+        return cuda_fail(e, "pinned staging buffers");
+      }
+    }
+  }
+  const size_t cap = std::min(limit, chunk);
   void* ws = nullptr;
-  const size_t bytes = n * 2 + limit * 8 + 64;
-  cudaError_t e = cudaMalloc(&ws, bytes);
+  u16m::keep_pool_memory();
+  e = cudaMallocAsync(&ws, cap * sizeof(unsigned long long) + 64, p->comp);
   if (e != cudaSuccess) return cuda_fail(e, "workspace");
   auto* d_off = static_cast<unsigned long long*>(ws);
-  auto* d_cnt = d_off + limit;
-  auto* d_in = reinterpret_cast<uint16_t*>(d_cnt + 4);
-  e = cudaMemcpy(d_in, in, n * 2, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = u16m::launch_unpaired_offsets(d_in, n, limit, d_off, d_cnt, nullptr);
-  unsigned long long cnt = 0;
-  if (e == cudaSuccess) e = cudaMemcpy(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess && cnt) e = cudaMemcpy(offsets_out, d_off, cnt * 8, cudaMemcpyDeviceToHost);
-  cudaFree(ws);
+  auto* d_cnt = d_off + cap;
+  const size_t nchunks = (n + chunk - 1) / chunk;
+  auto load = [&](size_t c) -> cudaError_t {  // H2D of chunk c into device slot c % 2
+    const int k = static_cast<int>(c % 2);
+    const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
+    const uint16_t* src = in + c0;
+    if (!pinned) {
+      CopyPool::get().copy(p->stage[k], src, len * sizeof(uint16_t));
+      src = p->stage[k];
+    }
+    const cudaError_t r = cudaMemcpyAsync(p->dbuf[k], src, len * 2, cudaMemcpyHostToDevice, p->h2d);
+    if (r == cudaSuccess) cudaEventRecord(p->loaded[k], p->h2d);
+    return r;
+  };
+  size_t found = 0;
+  e = load(0);
+  for (size_t c = 0; c < nchunks && e == cudaSuccess; c++) {
+    const int k = static_cast<int>(c % 2);
+    const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
+    // the next chunk's slot was last read by chunk c-1's scan, finished below
+    if (c + 1 < nchunks) e = load(c + 1);
+    if (e != cudaSuccess) break;
+    cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
+    const int32_t left = c0 > 0 ? in[c0 - 1] : -1;
+    const int32_t right = c0 + len < n ? in[c0 + len] : -1;
+    e = u16m::launch_unpaired_offsets(p->dbuf[k], len, std::min(limit - found, cap), d_off, d_cnt, p->comp,
+                                      left, right);
+    if (e != cudaSuccess) break;
+    unsigned long long cnt = 0;
+    e = cudaMemcpyAsync(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, p->comp);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
+    if (e == cudaSuccess && cnt) e = cudaMemcpy(offsets_out + found, d_off, cnt * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) break;
+    for (size_t i = 0; i < cnt; i++) offsets_out[found + i] += c0;  // chunk-relative -> buffer offsets
+    found += cnt;
+    if (found >= limit) break;
+  }
+  const cudaError_t f = cudaStreamSynchronize(p->h2d);  // a prefetched chunk may still read `in`
+  cudaFreeAsync(ws, p->comp);
+  cudaStreamSynchronize(p->comp);
   if (e != cudaSuccess) return cuda_fail(e, "unpaired offsets");
-  *count_out = static_cast<size_t>(cnt);
+  if (f != cudaSuccess) return cuda_fail(f, "unpaired offsets");
+  *count_out = found;
   return U16M_OK;
 }
 

@@ -51,7 +51,7 @@ cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out,
 void keep_pool_memory();
 // Count of units repair would rewrite, read-only stream kernel (adds to *count).
 cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream,
-                                uint32_t* half_tile_counts = nullptr);
+                                uint32_t* half_tile_counts = nullptr, int32_t left = -1, int32_t right = -1);
 // Batched form with the buffer length known: tile table pre-pass + one tile
 // per CTA (u16m_stream.cu). offsets[S] <= n_units.
 bool batched_tiles_enabled();
@@ -67,9 +67,11 @@ cudaError_t launch_fix_bytes(const void* in, size_t n, void* out, bool big_endia
 cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long long* count_out,
                                   cudaStream_t stream);
 
+// left/right: halo units around [in, in+n) (-1 = outside the buffer), so a
+// caller can scan a long host buffer chunk by chunk.
 cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
                                     unsigned long long* offsets_out, unsigned long long* count_out,
-                                    cudaStream_t stream);
+                                    cudaStream_t stream, int32_t left = -1, int32_t right = -1);
 
 unsigned long long launch_count();
 void note_launch();

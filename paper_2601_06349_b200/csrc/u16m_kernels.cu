@@ -522,11 +522,11 @@ __global__ void __launch_bounds__(1024) tile_prefix_kernel(const uint32_t* count
 
 cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
                                     unsigned long long* offsets_out, unsigned long long* count_out,
-                                    cudaStream_t stream) {
+                                    cudaStream_t stream, int32_t left, int32_t right) {
   cudaError_t e = cudaMemsetAsync(count_out, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess || n == 0 || limit == 0) return e;
   bool same = false;
-  const Span s = make_span(in, n, nullptr, -1, -1, nullptr, nullptr, &same);
+  const Span s = make_span(in, n, nullptr, left, right, nullptr, nullptr, &same);
   const uint64_t tiles = tiles_for(s);  // 8192-unit tiles of the emit pass
   const uint64_t halves = 2 * (((s.hi + 7) / 8 - s.lo / 8 + 2 * kCtaVecs - 1) / (2 * kCtaVecs));
   void* ws = nullptr;
@@ -540,7 +540,7 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   //    flight per thread) writes one count per half of its 16384-unit tile;
   // 2) exclusive prefix + the total; 3) emit on a persistent grid that stops
   //    at the first tile ranked past the limit.
-  e = launch_stream_count(in, n, nullptr, stream, counts);
+  e = launch_stream_count(in, n, nullptr, stream, counts, left, right);
   if (e == cudaSuccess) {
     tile_prefix_kernel<<<1, 1024, 0, stream>>>(counts, tiles, prefix, limit, count_out);
     g_launches.fetch_add(1, std::memory_order_relaxed);

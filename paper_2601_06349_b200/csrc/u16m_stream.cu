@@ -502,7 +502,7 @@ cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long lo
 // the rewrite count of every 8192-unit half tile instead of the total
 // (2 * ceil(n_vectors / 2048) entries).
 cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream,
-                                uint32_t* half_tile_counts) {
+                                uint32_t* half_tile_counts, int32_t left, int32_t right) {
   if (n == 0) return cudaSuccess;
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
@@ -512,7 +512,8 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
   s.out_units = nullptr;
   s.lo = ph;
   s.hi = ph + n;
-  s.left = s.right = -1;
+  s.left = left;
+  s.right = right;
   s.left_ptr = s.right_ptr = nullptr;
   s.tile_sel = kTilesAll;
   const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kSCtaVecs - 1) / kSCtaVecs;

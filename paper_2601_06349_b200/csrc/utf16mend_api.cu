@@ -173,18 +173,18 @@ void fix_scalar(char16_t* out, const char16_t* in, std::size_t n) {
 bool is_well_formed(std::span<const char16_t> in) {
   if (in.empty()) return true;
   const auto* i = reinterpret_cast<const uint16_t*>(in.data());
-  DeviceBuf cnt(sizeof(unsigned long long));
   if (is_device(i)) {
+    DeviceBuf cnt(sizeof(unsigned long long));
     check(u16m_count_unpaired(i, in.size(), cnt.as<unsigned long long>(), nullptr));
-  } else {
-    DeviceBuf d(in.size_bytes());
-    copy(d.p, i, in.size_bytes(), cudaMemcpyHostToDevice);
-    check(u16m_count_unpaired(d.as<uint16_t>(), in.size(), cnt.as<unsigned long long>(), nullptr));
-    sync_default();
+    unsigned long long c = 0;
+    copy(&c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost);
+    return c == 0;
   }
-  unsigned long long c = 0;
-  copy(&c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost);
-  return c == 0;
+  // Host memory: chunked scan that stops at the first unpaired surrogate.
+  unsigned long long first = 0;
+  size_t found = 0;
+  check(u16m_unpaired_offsets_host(i, in.size(), 1, &first, &found));
+  return found == 0;
 }
 
 std::vector<std::size_t> unpaired_surrogate_offsets(std::span<const char16_t> in, std::size_t limit) {
@@ -192,20 +192,22 @@ std::vector<std::size_t> unpaired_surrogate_offsets(std::span<const char16_t> in
   if (in.empty() || limit == 0) return result;
   const size_t cap = limit < in.size() ? limit : in.size();
   const auto* i = reinterpret_cast<const uint16_t*>(in.data());
-  DeviceBuf cnt(sizeof(unsigned long long)), offs(cap * sizeof(unsigned long long));
-  DeviceBuf d(is_device(i) ? 0 : in.size_bytes());
-  const uint16_t* src = i;
-  if (!is_device(i)) {
-    copy(d.p, i, in.size_bytes(), cudaMemcpyHostToDevice);
-    src = d.as<uint16_t>();
+  std::vector<unsigned long long> tmp;
+  if (is_device(i)) {
+    DeviceBuf cnt(sizeof(unsigned long long)), offs(cap * sizeof(unsigned long long));
+    check(u16m_unpaired_offsets(i, in.size(), cap, offs.as<unsigned long long>(), cnt.as<unsigned long long>(),
+                                nullptr));
+    sync_default();
+    unsigned long long c = 0;
+    copy(&c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost);
+    tmp.resize(c);
+    copy(tmp.data(), offs.p, c * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  } else {
+    tmp.resize(cap);
+    size_t c = 0;
+    check(u16m_unpaired_offsets_host(i, in.size(), cap, tmp.data(), &c));
+    tmp.resize(c);
   }
-  check(u16m_unpaired_offsets(src, in.size(), cap, offs.as<unsigned long long>(),
-                              cnt.as<unsigned long long>(), nullptr));
-  sync_default();
-  unsigned long long c = 0;
-  copy(&c, cnt.p, sizeof(c), cudaMemcpyDeviceToHost);
-  std::vector<unsigned long long> tmp(c);
-  copy(tmp.data(), offs.p, c * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   result.assign(tmp.begin(), tmp.end());
   return result;
 }

@@ -610,3 +610,32 @@ def test_dlpack_producers_zero_copy(P, cuda):
     offs = torch.tensor([0, 2, 7], dtype=torch.int64, device="cuda")
     got = P.to_well_formed_batched(_DLPackArray(t), _DLPackArray(offs))
     assert (host(got) == O.fix_batched(x, np.array([0, 2, 7]))).all()
+
+
+def test_host_scan_chunks(P, cuda):
+    """u16m_unpaired_offsets_host (CLI check, is_well_formed, Python offsets on
+    bytes): chunked over 32 MiB pieces with halos — a pair straddling a chunk
+    edge is valid, lone units at chunk edges are found; pinned and pageable;
+    early exit at `limit`."""
+    import ctypes
+    C = 16 << 20                       # default pipeline chunk in units
+    n = 3 * C + 777
+    x = np.full(n, 0x41, np.uint16)
+    x[C - 1], x[C] = 0xD83D, 0xDE0A   # valid pair across the first chunk edge
+    lone = [0, 5, 2 * C - 1, 2 * C, 3 * C + 776]
+    for p_ in lone:
+        x[p_] = 0xDC00 if p_ % 2 else 0xD800
+    x[2 * C], x[2 * C - 1] = 0xDC00, 0xDC00  # L|L across the second edge: both lone
+    exp = O.unpaired_offsets(x)
+    assert exp == sorted(set(lone))
+    assert P.unpaired_surrogate_offsets(x.tobytes()) == exp
+    for lim in (1, 2, 3, 4, 5, 100):
+        assert P.unpaired_surrogate_offsets(x.tobytes(), lim) == exp[:lim]
+    assert not P.is_well_formed_utf16le(x.tobytes())
+    assert P.is_well_formed_utf16le(O.fix_scalar(x).tobytes())
+    L = P._lib.raw()
+    pin = torch.from_numpy(x.view(np.int16)).pin_memory()
+    out = np.zeros(10, np.uint64)
+    cnt = ctypes.c_size_t(0)
+    assert L.u16m_unpaired_offsets_host(pin.data_ptr(), n, 10, out.ctypes.data, ctypes.byref(cnt)) == 0
+    assert out[: cnt.value].tolist() == exp
