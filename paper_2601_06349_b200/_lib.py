@@ -259,14 +259,12 @@ def fix_utf16le(data, kernel: Optional[str] = None) -> bytes:
     mv = _check_bytes(data)
     _kernel_from_name(kernel)
     n = mv.nbytes // 2
-    out = bytearray(mv.nbytes)
     if n == 0:
-        return bytes(out)
-    src = bytearray(mv) if mv.readonly else mv
-    in_buf = (ctypes.c_char * mv.nbytes).from_buffer(src)
-    out_buf = (ctypes.c_char * mv.nbytes).from_buffer(out)
-    _check(_L.u16m_to_well_formed_host(ctypes.addressof(in_buf), n, ctypes.addressof(out_buf)))
-    return bytes(out)
+        return b""
+    src = _host_ptr(mv)                         # read in place, no Python-side copy
+    out, addr = _new_bytes(mv.nbytes)
+    _check(_L.u16m_to_well_formed_host(src.ctypes.data, n, addr))
+    return out
 
 
 def fix_str(text: str, kernel: Optional[str] = None) -> str:
@@ -274,6 +272,33 @@ def fix_str(text: str, kernel: Optional[str] = None) -> str:
     (proj/python/utf16mend/__init__.py:24-31)."""
     data = text.encode("utf-16-le", "surrogatepass")
     return fix_utf16le(data, kernel).decode("utf-16-le")
+
+
+_PyBytes_FromStringAndSize = ctypes.pythonapi.PyBytes_FromStringAndSize
+_PyBytes_FromStringAndSize.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
+_PyBytes_FromStringAndSize.restype = ctypes.py_object
+_PyBytes_AsString = ctypes.pythonapi.PyBytes_AsString
+_PyBytes_AsString.argtypes = [ctypes.py_object]
+_PyBytes_AsString.restype = ctypes.c_void_p
+
+
+def _new_bytes(nbytes: int):
+    """A fresh, uninitialised `bytes` object and the address of its buffer, for
+    the C ABI to write the result into before the object is returned (the
+    reference's bindings also hand back bytes, module.cpp:54-64). Skips the
+    zero-fill of a bytearray and the final bytes() copy — on a 512 MiB
+    result those two passes cost 450 ms against 20 ms for the repair itself."""
+    out = _PyBytes_FromStringAndSize(None, nbytes)
+    return out, _PyBytes_AsString(out)
+
+
+def _host_ptr(mv: memoryview):
+    """A uint8 numpy view of the caller's bytes (zero-copy; `.ctypes.data` is
+    the address the C ABI reads), copied only when not 2-byte aligned."""
+    import numpy as np
+
+    src = np.frombuffer(mv, dtype=np.uint8)
+    return src.copy() if src.ctypes.data % 2 else src
 
 
 def _host_offsets(data, limit: int) -> list[int]:
@@ -287,9 +312,7 @@ def _host_offsets(data, limit: int) -> list[int]:
     if n == 0 or limit <= 0:
         return []
     cap = min(int(limit), n)
-    src = np.frombuffer(mv, dtype=np.uint8)
-    if src.ctypes.data % 2:                     # the C ABI needs whole-unit alignment
-        src = src.copy()
+    src = _host_ptr(mv)
     out = np.empty(cap, dtype=np.uint64)
     cnt = ctypes.c_size_t(0)
     _check(_L.u16m_unpaired_offsets_host(src.ctypes.data, n, cap, out.ctypes.data, ctypes.byref(cnt)))
@@ -330,17 +353,15 @@ def fix_utf16_bytes(data, byte_order: str = "le") -> tuple[bytes, int]:
     mv = _check_bytes(data)
     if byte_order not in ("le", "be"):
         raise ValueError("byte_order must be 'le' or 'be'")
-    out = bytearray(mv.nbytes)
     n = mv.nbytes // 2
     if n == 0:
-        return bytes(out), 0
-    src = bytearray(mv)
-    a = (ctypes.c_char * len(src)).from_buffer(src)
-    b = (ctypes.c_char * len(out)).from_buffer(out)
+        return b"", 0
+    src = _host_ptr(mv)
+    out, addr = _new_bytes(mv.nbytes)
     cnt = ctypes.c_ulonglong(0)
-    _check(_L.u16m_fix_utf16_bytes_host(ctypes.addressof(a), n, ctypes.addressof(b), 1 if byte_order == "be" else 0,
+    _check(_L.u16m_fix_utf16_bytes_host(src.ctypes.data, n, addr, 1 if byte_order == "be" else 0,
                                         ctypes.byref(cnt)))
-    return bytes(out), int(cnt.value)
+    return out, int(cnt.value)
 
 
 def to_well_formed_bytes(x: torch.Tensor, out: Optional[torch.Tensor] = None, big_endian: bool = False,

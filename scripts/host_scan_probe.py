@@ -22,3 +22,11 @@ for name, fn in (("is_well_formed(clean 512 MiB)", lambda: P.is_well_formed_utf1
         fn()
         best = min(best, time.perf_counter() - t)
     print(f"{name:45s} {best * 1e3:8.2f} ms  {2 * n / best / 1e9:6.1f} GB/s", flush=True)
+for name, fn in (("fix_utf16le(C1 512 MiB bytes)", lambda: P.fix_utf16le(bad)),
+                 ("fix_utf16_bytes(C1, be)", lambda: P.fix_utf16_bytes(bad, "be"))):
+    best = 1e9
+    for _ in range(3):
+        t = time.perf_counter()
+        fn()
+        best = min(best, time.perf_counter() - t)
+    print(f"{name:45s} {best * 1e3:8.2f} ms  {2 * n / best / 1e9:6.1f} GB/s", flush=True)
