@@ -16,6 +16,7 @@
 
 #include <cerrno>
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -39,9 +40,25 @@ struct usage_error : std::runtime_error {
 enum class order { little, big };
 
 std::vector<uint8_t> read_file(const std::string& path) {
-  std::ifstream f(path, std::ios::binary);
+  // Block reads (a byte-wise istreambuf_iterator copy ran at well under 1 GB/s).
+  std::FILE* f = std::fopen(path.c_str(), "rb");
   if (!f) throw std::runtime_error(path + ": " + std::strerror(errno));
-  return std::vector<uint8_t>(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  std::vector<uint8_t> buf;
+  if (std::fseek(f, 0, SEEK_END) == 0) {
+    const long size = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    if (size > 0) {
+      buf.resize(static_cast<size_t>(size));
+      buf.resize(std::fread(buf.data(), 1, buf.size(), f));
+    }
+  }
+  std::vector<uint8_t> blk(size_t(1) << 20);  // the rest (pipes, files that grew)
+  for (size_t got; (got = std::fread(blk.data(), 1, blk.size(), f)) > 0;)
+    buf.insert(buf.end(), blk.begin(), blk.begin() + static_cast<std::ptrdiff_t>(got));
+  const bool err = std::ferror(f) != 0;
+  std::fclose(f);
+  if (err) throw std::runtime_error(path + ": read failed");
+  return buf;
 }
 
 void write_file(const std::string& path, const std::vector<uint8_t>& bytes) {
