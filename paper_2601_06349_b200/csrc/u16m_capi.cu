@@ -233,8 +233,7 @@ HostPipe* pipe_for(int device, u16m_status* st) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&p->counter, sizeof(unsigned long long));
   for (int i = 0; i < kRing && e == cudaSuccess; i++) {
-    e = cudaMalloc(&p->dbuf[i], pipe_chunk_units() * sizeof(uint16_t));  // 8 x 32 MiB by default
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->loaded[i], cudaEventDisableTiming);
+    e = cudaEventCreateWithFlags(&p->loaded[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->repaired[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->drained[i], cudaEventDisableTiming);
   }
@@ -256,6 +255,26 @@ HostPipe* pipe_for(int device, u16m_status* st) {
   }
   g_pipes.push_back(p);
   return p;
+}
+
+// Device ring slot k / pinned bounce buffer k, allocated on first use at the
+// full chunk size (a one-chunk job never pays for the other slots: cudaHostAlloc
+// of 32 MiB alone takes tens of ms).
+cudaError_t ensure_dbuf(HostPipe* p, int k) {
+  if (p->dbuf[k]) return cudaSuccess;
+  return cudaMalloc(&p->dbuf[k], pipe_chunk_units() * sizeof(uint16_t));
+}
+
+cudaError_t ensure_stage(HostPipe* p, int k) {
+  if (p->stage[k]) return cudaSuccess;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p->stage[k]), pipe_chunk_units() * sizeof(uint16_t),
+                                cudaHostAllocDefault);
+  if (e == cudaSuccess && !p->staged[k]) e = cudaEventCreateWithFlags(&p->staged[k], cudaEventDisableTiming);
+  if (e != cudaSuccess && p->stage[k]) {
+    cudaFreeHost(p->stage[k]);
+    p->stage[k] = nullptr;
+  }
+  return e;
 }
 
 // Host-path mode (U16M_HOST_MODE). Measured on the B200 box (scripts/
@@ -524,16 +543,6 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
   // single-threaded staging of pageable copies (7 GB/s on a 512 MiB job).
   if (!is_pinned(in) || !is_pinned(out)) {
     const size_t chunk = pipe_chunk_units();
-    for (int i = 0; i < kStage; i++) {
-      if (p->stage[i]) continue;
-      e = cudaHostAlloc(reinterpret_cast<void**>(&p->stage[i]), chunk * sizeof(uint16_t), cudaHostAllocDefault);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->staged[i], cudaEventDisableTiming);
-      if (e != cudaSuccess) {
-        if (p->stage[i]) cudaFreeHost(p->stage[i]);
-        p->stage[i] = nullptr;
-        return cuda_fail(e, "pinned staging buffers");
-      }
-    }
     CopyPool& pool = CopyPool::get();
     const size_t nchunks = (n + chunk - 1) / chunk;
     auto copy_out = [&](size_t c) -> cudaError_t {
@@ -550,6 +559,9 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
         e = copy_out(c - kStage);  // frees slot k (its D2H is complete)
         if (e != cudaSuccess) return cuda_fail(e, "staged D2H");
       }
+      e = ensure_stage(p, k);
+      if (e == cudaSuccess) e = ensure_dbuf(p, k);
+      if (e != cudaSuccess) return cuda_fail(e, "staging buffers");
       const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
       // Halo units come from the caller's input. In place, chunks up to
       // c - kStage have been written back by now, never c-1 or c+1 (kStage
@@ -586,6 +598,8 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
   // Write-back mode (A/B): the host buffer already holds the input, so
   // instead of a D2H copy of every chunk the kernel stores only the 32-byte
   // groups that hold a rewrite straight into host memory.
+  e = ensure_dbuf(p, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "device chunk buffer");
   const bool writeback = in == out && dout != nullptr && host_mode() == kHostWriteback &&
                          ((reinterpret_cast<uintptr_t>(dout) ^ reinterpret_cast<uintptr_t>(p->dbuf[0])) & 15u) == 0;
   size_t c = 0;
@@ -602,6 +616,8 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
       e = cudaStreamWaitEvent(p->h2d, writeback ? p->repaired[k] : p->drained[k], 0);
       if (e != cudaSuccess) return cuda_fail(e, "pipeline wait");
     }
+    e = ensure_dbuf(p, k);
+    if (e != cudaSuccess) return cuda_fail(e, "device chunk buffer");
     e = cudaMemcpyAsync(p->dbuf[k], in + c0, len * 2, cudaMemcpyHostToDevice, p->h2d);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
     cudaEventRecord(p->loaded[k], p->h2d);
@@ -667,18 +683,7 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
   // is_well_formed for 1), so an ill-formed buffer is rarely read to its end.
   const bool pinned = is_pinned(in);
   const size_t chunk = pipe_chunk_units();
-  if (!pinned) {
-    for (int i = 0; i < 2; i++) {
-      if (p->stage[i]) continue;
-      e = cudaHostAlloc(reinterpret_cast<void**>(&p->stage[i]), chunk * sizeof(uint16_t), cudaHostAllocDefault);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->staged[i], cudaEventDisableTiming);
-      if (e != cudaSuccess) {
-        if (p->stage[i]) cudaFreeHost(p->stage[i]);
-        p->stage[i] = nullptr;
-        return cuda_fail(e, "pinned staging buffers");
-      }
-    }
-  }
+
   const size_t cap = std::min(limit, chunk);
   void* ws = nullptr;
   u16m::keep_pool_memory();
@@ -689,13 +694,16 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
   const size_t nchunks = (n + chunk - 1) / chunk;
   auto load = [&](size_t c) -> cudaError_t {  // H2D of chunk c into device slot c % 2
     const int k = static_cast<int>(c % 2);
+    cudaError_t r = ensure_dbuf(p, k);
+    if (r == cudaSuccess && !pinned) r = ensure_stage(p, k);
+    if (r != cudaSuccess) return r;
     const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
     const uint16_t* src = in + c0;
     if (!pinned) {
       CopyPool::get().copy(p->stage[k], src, len * sizeof(uint16_t));
       src = p->stage[k];
     }
-    const cudaError_t r = cudaMemcpyAsync(p->dbuf[k], src, len * 2, cudaMemcpyHostToDevice, p->h2d);
+    r = cudaMemcpyAsync(p->dbuf[k], src, len * 2, cudaMemcpyHostToDevice, p->h2d);
     if (r == cudaSuccess) cudaEventRecord(p->loaded[k], p->h2d);
     return r;
   };
