@@ -147,6 +147,11 @@ u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out,
                                       unsigned long long* replacements);
 u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,
                                        unsigned long long* offsets_out, size_t* count_out);
+/* Batched form on host memory (behind the C++ to_well_formed_batched on host
+ * spans): `in`/`out` hold n_units units (equal or disjoint), `offsets` (host)
+ * num_strings + 1 non-decreasing entries within [0, n_units]. Synchronous. */
+u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units, const int64_t* offsets,
+                                             size_t num_strings, uint16_t* out);
 
 const char* u16m_status_string(u16m_status status);
 const char* u16m_last_error(void);

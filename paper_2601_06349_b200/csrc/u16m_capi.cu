@@ -277,6 +277,61 @@ cudaError_t ensure_stage(HostPipe* p, int k) {
   return e;
 }
 
+// Whole-buffer copies between host memory and a device buffer for the host
+// entry points that need the data resident at once (batched). Pinned host
+// memory is copied directly; pageable memory goes through two pinned bounce
+// buffers, the CopyPool filling (draining) one while the copy engine moves
+// the other. Synchronous.
+cudaError_t h2d_staged(HostPipe* p, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  if (is_pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, p->h2d) == cudaSuccess
+                                 ? cudaStreamSynchronize(p->h2d) : cudaGetLastError();
+  const size_t cb = pipe_chunk_units() * sizeof(uint16_t);
+  cudaError_t e = cudaSuccess;
+  size_t i = 0;
+  for (size_t off = 0; off < bytes && e == cudaSuccess; off += cb, i++) {
+    const int k = static_cast<int>(i % 2);
+    const size_t len = std::min(cb, bytes - off);
+    e = ensure_stage(p, k);
+    if (e == cudaSuccess && i >= 2) e = cudaEventSynchronize(p->staged[k]);  // its previous DMA is done
+    if (e != cudaSuccess) break;
+    CopyPool::get().copy(p->stage[k], static_cast<const char*>(src) + off, len);
+    e = cudaMemcpyAsync(static_cast<char*>(dst) + off, p->stage[k], len, cudaMemcpyHostToDevice, p->h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(p->staged[k], p->h2d);
+  }
+  const cudaError_t f = cudaStreamSynchronize(p->h2d);
+  return e != cudaSuccess ? e : f;
+}
+
+cudaError_t d2h_staged(HostPipe* p, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  if (is_pinned(dst)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, p->d2h) == cudaSuccess
+                                 ? cudaStreamSynchronize(p->d2h) : cudaGetLastError();
+  const size_t cb = pipe_chunk_units() * sizeof(uint16_t);
+  const size_t nchunks = (bytes + cb - 1) / cb;
+  cudaError_t e = cudaSuccess;
+  auto issue = [&](size_t i) {  // DMA chunk i into bounce buffer i % 2
+    const int k = static_cast<int>(i % 2);
+    const size_t off = i * cb, len = std::min(cb, bytes - off);
+    cudaError_t r = ensure_stage(p, k);
+    if (r == cudaSuccess)
+      r = cudaMemcpyAsync(p->stage[k], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, p->d2h);
+    if (r == cudaSuccess) r = cudaEventRecord(p->staged[k], p->d2h);
+    return r;
+  };
+  e = issue(0);
+  for (size_t i = 0; i < nchunks && e == cudaSuccess; i++) {
+    const int k = static_cast<int>(i % 2);
+    if (i + 1 < nchunks) e = issue(i + 1);  // the other buffer was drained in the previous iteration
+    if (e == cudaSuccess) e = cudaEventSynchronize(p->staged[k]);
+    if (e != cudaSuccess) break;
+    const size_t off = i * cb, len = std::min(cb, bytes - off);
+    CopyPool::get().copy(static_cast<char*>(dst) + off, p->stage[k], len);
+  }
+  const cudaError_t f = cudaStreamSynchronize(p->d2h);
+  return e != cudaSuccess ? e : f;
+}
+
 // Host-path mode (U16M_HOST_MODE). Measured on the B200 box (scripts/
 // e2e_probe.py, 512 MiB, input GB/s, in place / copy; the in-place input was
 // restored by a CPU memcpy right before each call, which alone costs the H2D
@@ -657,6 +712,48 @@ u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out,
     return fail(U16M_ERR_INVALID_ARGUMENT, "byte_order must be U16M_LITTLE_ENDIAN or U16M_BIG_ENDIAN");
   return host_pipeline(static_cast<const uint16_t*>(in), n_units, static_cast<uint16_t*>(out), byte_order,
                        replacements);
+}
+
+u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units, const int64_t* offsets,
+                                             size_t num_strings, uint16_t* out) {
+  if (offsets == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "offsets is null");
+  U16M_TRY(check_pair(in, n_units, out));
+  if (num_strings == 0 || n_units == 0) {
+    if (out != in && n_units) std::memcpy(out, in, n_units * sizeof(uint16_t));
+    return U16M_OK;
+  }
+  for (size_t s = 0; s < num_strings; s++)
+    if (offsets[s] < 0 || offsets[s + 1] < offsets[s] || static_cast<size_t>(offsets[s + 1]) > n_units)
+      return fail(U16M_ERR_INVALID_ARGUMENT, "offsets must be non-decreasing within the buffer");
+  U16M_TRY(check_device_present());
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(g_pipe_mu);
+  u16m_status st = U16M_OK;
+  HostPipe* p = pipe_for(dev, &st);
+  if (p == nullptr) return st;
+  u16m::keep_pool_memory();
+  const size_t data_bytes = n_units * sizeof(uint16_t), off_bytes = (num_strings + 1) * sizeof(int64_t);
+  const size_t off_at = (data_bytes + 15) / 16 * 16;
+  void* ws = nullptr;
+  e = cudaMallocAsync(&ws, off_at + off_bytes, p->comp);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
+  if (e != cudaSuccess) return cuda_fail(e, "device buffer");
+  auto* d_data = static_cast<uint16_t*>(ws);
+  auto* d_off = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + off_at);
+  e = h2d_staged(p, d_data, in, data_bytes);
+  if (e == cudaSuccess) e = h2d_staged(p, d_off, offsets, off_bytes);
+  if (e == cudaSuccess) {
+    const cudaError_t k = u16m::launch_batched_tiles(d_data, n_units, d_off, num_strings, d_data, p->comp);
+    e = k != cudaSuccess ? k : cudaStreamSynchronize(p->comp);
+  }
+  if (e == cudaSuccess) e = d2h_staged(p, out, d_data, data_bytes);
+  cudaFreeAsync(ws, p->comp);
+  const cudaError_t f = cudaStreamSynchronize(p->comp);
+  if (e != cudaSuccess) return cuda_fail(e, "batched host repair");
+  if (f != cudaSuccess) return cuda_fail(f, "batched host repair");
+  return U16M_OK;
 }
 
 u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,

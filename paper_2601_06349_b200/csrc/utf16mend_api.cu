@@ -154,14 +154,7 @@ void to_well_formed_batched(std::span<const char16_t> in, std::span<const std::i
     sync_default();
     return;
   }
-  for (size_t s = 0; s < S; s++)
-    if (offsets[s] < 0 || offsets[s + 1] < offsets[s] || static_cast<size_t>(offsets[s + 1]) > in.size())
-      throw std::invalid_argument("to_well_formed_batched: offsets must be non-decreasing within the buffer");
-  DeviceBuf d(in.size_bytes()), doff(offsets.size_bytes());
-  copy(d.p, i, in.size_bytes(), cudaMemcpyHostToDevice);
-  copy(doff.p, offsets.data(), offsets.size_bytes(), cudaMemcpyHostToDevice);
-  check(u16m_to_well_formed_batched_n(d.as<uint16_t>(), in.size(), doff.as<int64_t>(), S, d.as<uint16_t>(), nullptr));
-  copy(o, d.p, in.size_bytes(), cudaMemcpyDeviceToHost);
+  check(u16m_to_well_formed_batched_host(i, in.size(), offsets.data(), S, o));
 }
 
 void fix_scalar(std::span<const char16_t> in, std::span<char16_t> out) { to_well_formed(in, out); }

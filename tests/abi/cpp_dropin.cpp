@@ -3,6 +3,7 @@
 // driver.hpp and linked to libu16m.so. Exit codes: 0 = repaired correctly,
 // 3 = std::runtime_error (no CUDA device: the path has no CPU fallback),
 // 1 = wrong result, 2 = wrong exception.
+#include <cstdint>
 #include <cstdio>
 #include <optional>
 #include <span>
@@ -51,6 +52,17 @@ int main() {
     if (is_well_formed(in) || !is_well_formed(expected)) return 1;
     if (unpaired_surrogate_offsets(in) != std::vector<std::size_t>{10, 21}) return 1;
     if (unpaired_surrogate_offsets(in, 1) != std::vector<std::size_t>{10}) return 1;
+    // batched on host vectors: strings [0,11) [11,22) [22,31) — the lone units stay lone
+    std::vector<char16_t> bo(in.size());
+    const std::vector<std::int64_t> offs{0, 11, 22, 31};
+    to_well_formed_batched(in, offs, bo);
+    if (bo != expected) return 1;
+    try {
+      const std::vector<std::int64_t> bad{0, 20, 11, 31};
+      to_well_formed_batched(in, bad, bo);
+      return 2;
+    } catch (const std::invalid_argument&) {
+    }
     std::printf("repaired %s\n", to_string(select_kernel()).c_str());
     return 0;
   } catch (const std::runtime_error& e) {

@@ -639,3 +639,31 @@ def test_host_scan_chunks(P, cuda):
     cnt = ctypes.c_size_t(0)
     assert L.u16m_unpaired_offsets_host(pin.data_ptr(), n, 10, out.ctypes.data, ctypes.byref(cnt)) == 0
     assert out[: cnt.value].tolist() == exp
+
+
+def test_batched_host_staged(P, cuda):
+    """u16m_to_well_formed_batched_host (behind the C++ batched API on host
+    spans): pageable and pinned buffers over several 32 MiB bounce chunks,
+    copy and in place, strings crossing chunk edges."""
+    import ctypes
+    rng = np.random.default_rng(31)
+    n = (16 << 20) * 3 + 999
+    x = O.gen_config(1, n, seed=31)
+    cuts = np.unique(np.concatenate([[5, n - 3, 16 << 20, (16 << 20) + 1], rng.integers(5, n - 3, 20000)]))
+    offs = cuts.astype(np.int64)
+    e = O.fix_batched(x, offs)
+    L = P._lib.raw()
+    L.u16m_to_well_formed_batched_host.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                                    ctypes.c_size_t, ctypes.c_void_p]
+    src = x.view(np.int16).copy()
+    out = np.empty_like(src)
+    assert L.u16m_to_well_formed_batched_host(src.ctypes.data, n, offs.ctypes.data, offs.size - 1, out.ctypes.data) == 0
+    assert (out.view(np.uint16) == e).all()
+    assert L.u16m_to_well_formed_batched_host(src.ctypes.data, n, offs.ctypes.data, offs.size - 1, src.ctypes.data) == 0
+    assert (src.view(np.uint16) == e).all()
+    pin = torch.from_numpy(x.view(np.int16).copy()).pin_memory()
+    assert L.u16m_to_well_formed_batched_host(pin.data_ptr(), n, offs.ctypes.data, offs.size - 1, pin.data_ptr()) == 0
+    assert (pin.numpy().view(np.uint16) == e).all()
+    bad = offs.copy()
+    bad[3], bad[4] = bad[4], bad[3]
+    assert L.u16m_to_well_formed_batched_host(src.ctypes.data, n, bad.ctypes.data, bad.size - 1, out.ctypes.data) == 1
