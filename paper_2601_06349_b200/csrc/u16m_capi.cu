@@ -10,6 +10,7 @@
 // backend is missing, proj/src/bitmask_kernel.cpp:102-104).
 
 #include <cuda_runtime.h>
+#include <unistd.h>
 #include <immintrin.h>
 
 #include <algorithm>
@@ -156,6 +157,7 @@ class CopyPool {
     return *pool;
   }
   void copy(void* dst, const void* src, size_t bytes) {
+    if (getpid() != pid_) respawn();  // forked child: the workers did not survive the fork
     if (workers_ == 0 || bytes < (size_t(1) << 20)) {
       std::memcpy(dst, src, bytes);
       return;
@@ -177,20 +179,23 @@ class CopyPool {
   }
 
  private:
-  CopyPool() {
+  CopyPool() { respawn(); }
+  void respawn() {
+    pid_ = getpid();
+    pending_ = 0;
     const char* e = std::getenv("U16M_HOST_THREADS");
     int t = e ? std::atoi(e) : static_cast<int>(std::thread::hardware_concurrency());
     t = std::max(1, std::min(t, 16));
     workers_ = t - 1;
-    for (int i = 0; i < workers_; i++) std::thread([this, i] { run(i); }).detach();
+    const unsigned long long g = gen_;
+    for (int i = 0; i < workers_; i++) std::thread([this, i, g] { run(i, g); }).detach();
   }
   void piece(int i) {
     const size_t a = std::min(bytes_, static_cast<size_t>(i) * piece_);
     const size_t b = i == workers_ ? bytes_ : std::min(bytes_, a + piece_);
     if (b > a) copy_piece(dst_ + a, src_ + a, b - a);
   }
-  void run(int i) {
-    unsigned long long seen = 0;
+  void run(int i, unsigned long long seen) {
     for (;;) {
       {
         std::unique_lock<std::mutex> l(mu_);
@@ -205,6 +210,7 @@ class CopyPool {
   std::mutex mu_;
   std::condition_variable cv_, done_;
   int workers_ = 0, pending_ = 0;
+  pid_t pid_ = 0;
   unsigned long long gen_ = 0;
   char* dst_ = nullptr;
   const char* src_ = nullptr;
