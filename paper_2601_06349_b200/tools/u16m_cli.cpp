@@ -95,35 +95,44 @@ void check_status(u16m_status st) {
   if (st != U16M_OK) throw std::runtime_error(std::string(u16m_status_string(st)) + ": " + u16m_last_error());
 }
 
-// The reference decode contract: returns the unit bytes (BOM removed) in the
-// detected/explicit byte order.
-struct decoded {
-  std::vector<uint8_t> bytes;  // raw unit bytes, even length, BOM removed
+// Where the units of a raw UTF-16 file lie (decode's contract without the copy).
+struct layout {
+  size_t start = 0;    // 2 when a BOM is consumed
+  size_t n_units = 0;  // whole units after the BOM
   order byte_order = order::little;
   bool had_bom = false;
-  bool padded = false;
+  bool padded = false;  // a dangling final byte (only with --pad-final)
 };
 
-decoded decode(const std::vector<uint8_t>& in, std::optional<order> explicit_order, bool pad_final) {
-  decoded d;
-  size_t start = 0;
+layout locate(const std::vector<uint8_t>& in, std::optional<order> explicit_order, bool pad_final) {
+  layout l;
   const bool le_bom = in.size() >= 2 && in[0] == 0xFF && in[1] == 0xFE;
   const bool be_bom = in.size() >= 2 && in[0] == 0xFE && in[1] == 0xFF;
   if (explicit_order) {
-    d.byte_order = *explicit_order;
-    d.had_bom = (*explicit_order == order::little && le_bom) || (*explicit_order == order::big && be_bom);
+    l.byte_order = *explicit_order;
+    l.had_bom = (*explicit_order == order::little && le_bom) || (*explicit_order == order::big && be_bom);
   } else {
-    d.byte_order = be_bom ? order::big : order::little;
-    d.had_bom = le_bom || be_bom;
+    l.byte_order = be_bom ? order::big : order::little;
+    l.had_bom = le_bom || be_bom;
   }
-  if (d.had_bom) start = 2;
-  d.bytes.assign(in.begin() + static_cast<std::ptrdiff_t>(start), in.end());
-  if (d.bytes.size() % 2 != 0) {
+  l.start = l.had_bom ? 2 : 0;
+  const size_t body = in.size() - l.start;
+  if (body % 2 != 0) {
     if (!pad_final) throw std::runtime_error("truncated UTF-16: odd number of bytes (use --pad-final)");
-    d.bytes.pop_back();
-    d.padded = true;
+    l.padded = true;
   }
-  return d;
+  l.n_units = body / 2;
+  return l;
+}
+
+void write_parts(const std::string& path, std::initializer_list<std::pair<const uint8_t*, size_t>> parts) {
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw std::runtime_error(path + ": " + std::strerror(errno));
+  bool ok = true;
+  for (const auto& [p, n] : parts)
+    if (n) ok = ok && std::fwrite(p, 1, n, f) == n;
+  ok = std::fclose(f) == 0 && ok;
+  if (!ok) throw std::runtime_error(path + ": write failed");
 }
 
 std::vector<uint8_t> encode(const std::vector<uint8_t>& unit_bytes, order o, bool with_bom) {
@@ -207,24 +216,29 @@ int cmd_fix(int argc, char** argv) {
   check_env_kernel();
   const auto explicit_order = parse_order(a.get("--endianness", "auto"));
 
-  const auto bytes = read_file(path);
-  decoded d = decode(bytes, explicit_order, a.has("--pad-final"));
+  // The units are repaired where they lie in the file buffer (no decode /
+  // encode copies of the payload); the output is written as BOM + units
+  // (+ U+FFFD for a dangling byte), exactly what decode -> fix -> encode gives.
+  auto bytes = read_file(path);
+  const layout d = locate(bytes, explicit_order, a.has("--pad-final"));
   if (!explicit_order && !d.had_bom)
     std::cerr << "utf16mend: " << path << ": no BOM found, assuming little-endian\n";
   if (bom == "require" && !d.had_bom) throw std::runtime_error(path + ": BOM required but not present");
 
   unsigned long long replacements = 0;
-  const size_t n = d.bytes.size() / 2;
-  if (n > 0)
-    check_status(u16m_fix_utf16_bytes_host(d.bytes.data(), n, d.bytes.data(),
+  uint8_t* units = bytes.data() + d.start;
+  if (d.n_units > 0)
+    check_status(u16m_fix_utf16_bytes_host(units, d.n_units, units,
                                            d.byte_order == order::big ? U16M_BIG_ENDIAN : U16M_LITTLE_ENDIAN,
                                            &replacements));
+  std::vector<uint8_t> head, tail;
+  if (d.had_bom && bom != "strip") head = encode({}, d.byte_order, true);  // the BOM alone
   if (d.padded) {
-    append_fffd(d.bytes, d.byte_order);  // a dangling byte decodes as U+FFFD (codec contract)
+    append_fffd(tail, d.byte_order);  // a dangling byte decodes as U+FFFD (codec contract)
     replacements++;
   }
-  const bool with_bom = d.had_bom && bom != "strip";
-  write_file(in_place ? path : a.get("--output", ""), encode(d.bytes, d.byte_order, with_bom));
+  write_parts(in_place ? path : a.get("--output", ""),
+              {{head.data(), head.size()}, {units, 2 * d.n_units}, {tail.data(), tail.size()}});
   std::cout << replacements << (replacements == 1 ? " replacement\n" : " replacements\n");
   return 0;
 }
@@ -235,17 +249,23 @@ int cmd_check(int argc, char** argv) {
   const std::string path = a.pos[0];
   const auto explicit_order = parse_order(a.get("--endianness", "auto"));
   const auto bytes = read_file(path);
-  decoded d = decode(bytes, explicit_order, false);
+  const layout d = locate(bytes, explicit_order, false);
   if (!explicit_order && !d.had_bom)
     std::cerr << "utf16mend: " << path << ": no BOM found, assuming little-endian\n";
-  const size_t n = d.bytes.size() / 2;
-  std::vector<uint16_t> units(n);
-  for (size_t i = 0; i < n; i++)
-    units[i] = d.byte_order == order::little ? static_cast<uint16_t>(d.bytes[2 * i] | (d.bytes[2 * i + 1] << 8))
-                                             : static_cast<uint16_t>((d.bytes[2 * i] << 8) | d.bytes[2 * i + 1]);
+  const size_t n = d.n_units;
+  // Little-endian units are scanned where they lie in the file buffer; a
+  // big-endian file is byte-swapped into host order first.
+  std::vector<uint16_t> swapped;
+  const uint16_t* units = reinterpret_cast<const uint16_t*>(bytes.data() + d.start);
+  if (d.byte_order == order::big) {
+    swapped.resize(n);
+    const uint8_t* b = bytes.data() + d.start;
+    for (size_t i = 0; i < n; i++) swapped[i] = static_cast<uint16_t>((b[2 * i] << 8) | b[2 * i + 1]);
+    units = swapped.data();
+  }
   unsigned long long offs[10];
   size_t count = 0;
-  check_status(u16m_unpaired_offsets_host(units.data(), n, 10, offs, &count));
+  check_status(u16m_unpaired_offsets_host(units, n, 10, offs, &count));
   if (count == 0) {
     std::cout << path << ": well-formed\n";
     return 0;
