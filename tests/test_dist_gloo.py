@@ -93,3 +93,48 @@ def test_halo_pointer_offsets():
     assert pdist.halo_pointers(edges, 0) == (0, base + 8)
     assert pdist.halo_pointers(edges, 1) == (base + 4, base + 16)
     assert pdist.halo_pointers(edges, 3) == (base + 20, 0)
+
+
+def _peerhalo_worker(rank, world, port, fail_rank, q):
+    """PeerHalo's setup with the CUDA IPC pieces stubbed: when one rank cannot
+    map its neighbours, every rank must raise (so callers fall back together)
+    instead of the healthy ranks blocking in a barrier."""
+    import torch.multiprocessing.reductions as R
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def rebuild(*a):
+            if rank == fail_rank:
+                raise RuntimeError("cannot open IPC handle")
+            return torch.zeros(4, dtype=torch.int16)
+
+        R.reduce_tensor = lambda t: (rebuild, (None,) * 6 + (rank,) + (None,) * 8)
+        torch.cuda.can_device_access_peer = lambda a, b: True
+        torch.cuda.synchronize = lambda *a, **k: None
+        shard = torch.zeros(8, dtype=torch.int16)
+        try:
+            h = pdist.PeerHalo(shard)
+            q.put((rank, "ok", h.left_ptr != 0 or h.right_ptr != 0))
+        except RuntimeError as e:
+            q.put((rank, "raised", "PeerHalo setup failed" in str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 0, 1])
+def test_peer_halo_setup_failure_is_collective(fail_rank):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peerhalo_worker, args=(r, 2, port, fail_rank, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if fail_rank < 0:
+        assert res == [(0, "ok", True), (1, "ok", True)]
+    else:
+        assert res == [(0, "raised", True), (1, "raised", True)]
