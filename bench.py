@@ -326,7 +326,8 @@ def run_ours(args):
     def prepare():
         if pristine is not None:
             data.copy_(pristine)
-        _lib.l2_flush(flush)
+        if not args.warm:
+            _lib.l2_flush(flush)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -476,7 +477,8 @@ def run_ours(args):
         "config": {"workload": desc, "units_per_gpu": units, "mode": mode,
                    "parallelism": f"shard{world}" if distributed else "single",
                    "halo": (("ipc-peer-loads" if halo is not None else "nccl-allgather") if distributed else None),
-                   "l2": "flushed before every step (512 MiB streaming read) + restore outside the event pair",
+                   "l2": ("WARM: no L2 flush between steps (labelled warm number, not the headline)" if args.warm else
+                          "flushed before every step (512 MiB streaming read) + restore outside the event pair"),
                    "hbm_fraction_of_measured_peak": round((value / world) * (algo_bytes / in_bytes) / peak, 4),
                    "output_check_well_formed": bool(ok)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -530,6 +532,8 @@ def main():
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--warm", action="store_true",
+                    help="skip the L2 flush between steps (warm-cache number, SURVEY.md §8(d) C0; never the headline)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the sharded (NCCL halo exchange) step even at N=1 (under torchrun)")
