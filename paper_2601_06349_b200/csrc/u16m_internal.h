@@ -38,6 +38,8 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
 // in-place jobs; `s` from make_span, part as in launch_repair_part.
 struct Span;
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream);
+// Copy into an `out` whose 16-byte phase differs from in's (s from make_span).
+cudaError_t launch_stream_shift(Span s, uint16_t* out, int part, cudaStream_t stream);
 // Codec-fused form (u16m_stream.cu): same-phase buffers in little- or
 // big-endian byte order, optional device replacement counter (accumulated).
 cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long long* count, cudaStream_t stream);

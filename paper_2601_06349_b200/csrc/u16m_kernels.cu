@@ -413,6 +413,7 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
     return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
   }
   if ((in == out || same) && (choice == kChoiceAuto || choice == kChoiceLdg)) return launch_stream(s, part, stream);
+  if (choice == kChoiceAuto || choice == kChoiceLdg) return launch_stream_shift(s, out, part, stream);
   s.tile_sel = part;
   const uint64_t grid = part == kTilesAll ? ntiles
                         : part == kTilesEdges ? (ntiles < 2 ? ntiles : 2)

@@ -176,6 +176,133 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   }
 }
 
+// ---- copy between different 16-byte phases ----------------------------------
+// SURVEY.md §7 "arbitrary char16_t* alignment": when `out` and `in` differ mod
+// 16 bytes, unit a (in-aligned coordinates) lands at out-aligned coordinate
+// a + delta, delta = out phase - in phase. With s = delta mod 8 (1..7) and
+// q = (delta - s) / 8, out vector vi + q holds the last s units of repaired
+// vector vi-1 followed by the first 8-s units of repaired vector vi. In the
+// rolling layout vector vi-1 sits in the previous lane (lane 31 of the
+// previous k for lane 0), so each output vector is two register shuffles and
+// a compile-time funnel combine away; only the two vectors that straddle a
+// tile boundary are written unit by unit (half by each tile). Edge tiles (the
+// first and last of a job) write every unit individually.
+template <int S>
+__device__ __forceinline__ uint4 combine_units(const uint4& P, const uint4& C) {
+  const uint32_t W[8] = {P.x, P.y, P.z, P.w, C.x, C.y, C.z, C.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    const int i = 8 - S + 2 * w;  // first halfword of output word w in P ++ C
+    o[w] = (i & 1) ? __funnelshift_r(W[i >> 1], W[(i >> 1) + 1], 16) : W[i >> 1];
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+__device__ __forceinline__ uint4 shfl4(const uint4& v, int src, bool up) {
+  uint4 r;
+  if (up) {
+    r.x = __shfl_up_sync(kFull, v.x, 1), r.y = __shfl_up_sync(kFull, v.y, 1);
+    r.z = __shfl_up_sync(kFull, v.z, 1), r.w = __shfl_up_sync(kFull, v.w, 1);
+  } else {
+    r.x = __shfl_sync(kFull, v.x, src), r.y = __shfl_sync(kFull, v.y, src);
+    r.z = __shfl_sync(kFull, v.z, src), r.w = __shfl_sync(kFull, v.w, src);
+  }
+  return r;
+}
+
+template <int S>
+__global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int64_t q) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lane_off = threadIdx.x / 32 * kSWarpVecs + lane;
+  const uint64_t vbeg = s.lo / 8;
+  const uint64_t vend = (s.hi + 7) / 8;
+  const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
+  uint64_t tile = blockIdx.x;
+  if (s.tile_sel == kTilesEdges) tile = blockIdx.x == 0 ? 0 : ntiles - 1;
+  if (s.tile_sel == kTilesInterior) tile = blockIdx.x + 1;
+  if (tile >= ntiles) return;
+  const uint64_t tv0 = vbeg + tile * kSCtaVecs;
+  const bool interior = tv0 * 8 > s.lo && (tv0 + kSCtaVecs) * 8 < s.hi;
+  const uint64_t v0 = tv0 + lane_off;
+
+  uint4 v[kSV];
+  uint32_t halo = 0;
+  if (interior) {
+    const uint4* src = s.in + v0;
+#pragma unroll
+    for (int k = 0; k < kSV; k++) v[k] = ld_stream(src + k * 32);
+    const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
+    if (lane == 0) halo = src16[-1];
+    if (lane == 31) halo = src16[(kSV - 1) * 32 * 8 + 8];
+  } else {
+#pragma unroll
+    for (int k = 0; k < kSV; k++) {
+      const uint64_t vi = v0 + k * 32;
+      v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
+    }
+    const uint64_t warp_v0 = v0 - lane;
+    if (lane == 0) {
+      const int64_t a = static_cast<int64_t>(warp_v0 * 8) - 1;
+      halo = unit_at(s, a);
+    }
+    if (lane == 31) halo = unit_at(s, static_cast<int64_t>((warp_v0 + kSWarpVecs) * 8));
+#pragma unroll
+    for (int k = 0; k < kSV; k++) {
+      const uint64_t vi = v0 + k * 32;
+      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, v[k]);
+    }
+  }
+
+  Flags cur = classify8(v[0]);
+  uint32_t hp_carry = hflag_hi(halo);
+  const uint32_t halo_l = lflag_lo(halo);
+  uint4 carry = make_uint4(0, 0, 0, 0);  // lane 31's repaired vector k-1 (for lane 0)
+#pragma unroll
+  for (int k = 0; k < kSV; k++) {
+    Flags nxt;
+    if (k + 1 < kSV) nxt = classify8(v[k + 1]);
+    const uint32_t up = __shfl_sync(kFull, cur.H1, (lane + 31) & 31);
+    const uint32_t dn = __shfl_sync(kFull, cur.L0, (lane + 1) & 31);
+    uint32_t ln = dn;
+    if (k + 1 < kSV) {
+      const uint32_t dn_next = __shfl_sync(kFull, nxt.L0, (lane + 1) & 31);
+      if (lane == 31) ln = dn_next;
+    } else if (lane == 31) {
+      ln = halo_l;
+    }
+    const uint32_t hp = lane ? up : hp_carry;
+    hp_carry = up;
+    uint32_t B0, B1;
+    bad8(cur, hp, ln, B0, B1);
+    const uint4 r = blend(v[k], B0, B1);
+    const uint64_t vi = v0 + k * 32;
+    if (interior) {
+      uint4 prev = shfl4(r, 0, true);
+      if (lane == 0) prev = carry;
+      carry = shfl4(r, 31, false);
+      if (k == 0 && lane == 0) {
+        // head of a vector straddling the tile start: the previous tile writes the tail
+#pragma unroll
+        for (int j = 0; j < 8 - S; j++) s.out_units[vi * 8 + j - s.lo] = static_cast<uint16_t>(get_unit(r, j));
+      } else {
+        st_stream(s.out + static_cast<int64_t>(vi) + q, combine_units<S>(prev, r));
+      }
+      if (k == kSV - 1 && lane == 31) {
+#pragma unroll
+        for (int j = 8 - S; j < 8; j++) s.out_units[vi * 8 + j - s.lo] = static_cast<uint16_t>(get_unit(r, j));
+      }
+    } else if (vi < vend) {
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const uint64_t a = vi * 8 + j;
+        if (a >= s.lo && a < s.hi) s.out_units[a - s.lo] = static_cast<uint16_t>(get_unit(r, j));
+      }
+    }
+    if (k + 1 < kSV) cur = nxt;
+  }
+}
+
 // ---- batched form, non-persistent (buffer length known) ----------------------
 // Persistent grids measured 15-20 % slower than one-tile-per-CTA grids for
 // register-staged streaming (U16M_PERSIST), so the batched form also runs one
@@ -554,6 +681,38 @@ cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out,
   // here into a different buffer that already holds the input.
   if (big_endian) launch_codec_t<true, true>(s, g, count, stream);
   else launch_codec_t<true, false>(s, g, count, stream);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// Copy with out at a different 16-byte phase than in (see stream_shift_kernel).
+cudaError_t launch_stream_shift(Span s, uint16_t* out, int part, cudaStream_t stream) {
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
+  const int64_t pi = static_cast<int64_t>(s.lo);  // in phase (units); s.lo == phase for a plain job
+  const int64_t po = static_cast<int64_t>((oa & 15u) / 2);
+  const int64_t delta = po - pi;
+  const int sh = static_cast<int>(((delta % 8) + 8) % 8);
+  const int64_t q = (delta - sh) / 8;
+  s.out = reinterpret_cast<uint4*>(oa - 2 * po);
+  s.out_units = out;
+  const uint64_t vbeg = s.lo / 8, vend = (s.hi + 7) / 8;
+  const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
+  uint64_t grid = ntiles;
+  if (part == kTilesEdges) grid = ntiles < 2 ? ntiles : 2;
+  if (part == kTilesInterior) grid = ntiles > 2 ? ntiles - 2 : 0;
+  s.tile_sel = part;
+  if (grid == 0) return cudaSuccess;
+  const unsigned g = static_cast<unsigned>(grid);
+  switch (sh) {
+    case 1: stream_shift_kernel<1><<<g, kSThreads, 0, stream>>>(s, q); break;
+    case 2: stream_shift_kernel<2><<<g, kSThreads, 0, stream>>>(s, q); break;
+    case 3: stream_shift_kernel<3><<<g, kSThreads, 0, stream>>>(s, q); break;
+    case 4: stream_shift_kernel<4><<<g, kSThreads, 0, stream>>>(s, q); break;
+    case 5: stream_shift_kernel<5><<<g, kSThreads, 0, stream>>>(s, q); break;
+    case 6: stream_shift_kernel<6><<<g, kSThreads, 0, stream>>>(s, q); break;
+    case 7: stream_shift_kernel<7><<<g, kSThreads, 0, stream>>>(s, q); break;
+    default: return cudaErrorInvalidValue;  // same phase: launch_stream
+  }
   note_launch();
   return cudaGetLastError();
 }

@@ -667,3 +667,27 @@ def test_batched_host_staged(P, cuda):
     bad = offs.copy()
     bad[3], bad[4] = bad[4], bad[3]
     assert L.u16m_to_well_formed_batched_host(src.ctypes.data, n, bad.ctypes.data, bad.size - 1, out.ctypes.data) == 1
+
+
+def test_other_phase_copy_all_shifts(P, cuda):
+    """Copies whose output starts at a different 16-byte phase than the input
+    (the shifted-store kernel): every in/out phase pair, several CTA tiles,
+    units at every warp/tile straddle, nothing outside the output touched."""
+    rng = np.random.default_rng(17)
+    n = 16384 * 3 + 4099
+    x = rng.choice(ALPHABET, n)
+    x[16384 * np.arange(1, 4) - 1] = 0xD800     # H right before tile starts
+    x[2048 * np.arange(1, 20)] = 0xDC00          # L on warp-tile starts
+    e = O.stencil(x)
+    src_base = torch.zeros(n + 16, dtype=torch.int16, device="cuda")
+    out_base = torch.zeros(n + 32, dtype=torch.int16, device="cuda")
+    for pi in range(8):
+        src = src_base[pi:pi + n]
+        src.copy_(dev(x))
+        for po in range(8):
+            out_base.fill_(0x1234)
+            dst = out_base[8 + po:8 + po + n]
+            P.to_well_formed(src, out=dst)
+            assert (host(dst) == e).all(), (pi, po)
+            rest = torch.cat([out_base[:8 + po], out_base[8 + po + n:]])
+            assert bool((rest == 0x1234).all()), (pi, po)
