@@ -49,11 +49,16 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   if (s.tile_sel == kTilesEdges) nwork = ntiles < 2 ? ntiles : 2;
   if (s.tile_sel == kTilesInterior) nwork = ntiles > 2 ? ntiles - 2 : 0;
   uint32_t counted = 0;
+  uint64_t count_tile = 0;
   // One tile per CTA (persistent grids measured 15-20 % slower: profiles/README.md).
   for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-  uint64_t tile = w;
+  // The last tile goes first: a ragged last tile runs the edge code path
+  // (range patches, per-unit stores), whose cold instruction fetch made it
+  // finish ~14 us after everything else when it was dispatched last.
+  uint64_t tile = w == 0 ? ntiles - 1 : w - 1;
   if (s.tile_sel == kTilesEdges) tile = w == 0 ? 0 : ntiles - 1;
   if (s.tile_sel == kTilesInterior) tile = w + 1;
+  count_tile = tile;
   const uint64_t tv0 = vbeg + tile * kSCtaVecs;
   const bool interior = tv0 * 8 > s.lo && (tv0 + kSCtaVecs) * 8 < s.hi;
   const uint64_t v0 = tv0 + lane_off;  // this lane's vector k sits at v0 + 32k
@@ -164,8 +169,9 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
           c0 += warp_counts[w];
           c1 += warp_counts[w + kSThreads / 64];
         }
-        half_tile_counts[2 * blockIdx.x] = c0;
-        half_tile_counts[2 * blockIdx.x + 1] = c1;
+        // (one tile per CTA in this mode; the tile is not blockIdx.x: the last goes first)
+        half_tile_counts[2 * count_tile] = c0;
+        half_tile_counts[2 * count_tile + 1] = c1;
       } else {
         unsigned long long c = 0;
 #pragma unroll
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int6
   const uint64_t vbeg = s.lo / 8;
   const uint64_t vend = (s.hi + 7) / 8;
   const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
-  uint64_t tile = blockIdx.x;
+  uint64_t tile = blockIdx.x == 0 ? ntiles - 1 : blockIdx.x - 1;  // last (ragged) tile first
   if (s.tile_sel == kTilesEdges) tile = blockIdx.x == 0 ? 0 : ntiles - 1;
   if (s.tile_sel == kTilesInterior) tile = blockIdx.x + 1;
   if (tile >= ntiles) return;
@@ -383,8 +389,9 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   const uint64_t vbeg = s.lo / 8;
   const uint64_t vend = (s.hi + 7) / 8;
   const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
-  const uint64_t tile = blockIdx.x;
-  if (tile >= ntiles) return;
+  // the last (ragged, edge-path) tile first, as in stream_kernel
+  const uint64_t tile = blockIdx.x == 0 ? ntiles - 1 : blockIdx.x - 1;
+  if (blockIdx.x != 0 && tile >= ntiles - 1) return;
   const uint64_t tv0 = vbeg + tile * kSCtaVecs;
   const uint64_t wv0 = tv0 + threadIdx.x / 32 * kSWarpVecs;
   if (wv0 >= vend) return;  // warp tile past the job (no table entry either)
