@@ -60,7 +60,10 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   if (s.tile_sel == kTilesInterior) tile = w + 1;
   count_tile = tile;
   const uint64_t tv0 = vbeg + tile * kSCtaVecs;
-  const bool interior = tv0 * 8 > s.lo && (tv0 + kSCtaVecs) * 8 < s.hi;
+  // "interior": every vector of the tile lies fully inside [lo, hi) — also the
+  // first and last tile of a job whose ends are 16-byte aligned; only their
+  // outer halo units come from the halo rule instead of memory.
+  const bool interior = tv0 * 8 >= s.lo && (tv0 + kSCtaVecs) * 8 <= s.hi;
   const uint64_t v0 = tv0 + lane_off;  // this lane's vector k sits at v0 + 32k
 
   uint4 v[kSV];
@@ -77,8 +80,13 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
 #pragma unroll
     for (int k = 0; k < kSV; k++) v[k] = ld_stream(src + k * 32);
     const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
-    if (lane == 0) halo = to_mem<kBE>(src16[-1]);
-    if (lane == 31) halo = to_mem<kBE>(src16[(kSV - 1) * 32 * 8 + 8]);
+    const int64_t wa = static_cast<int64_t>((v0 - lane) * 8);  // the warp tile's first unit
+    if (lane == 0)
+      halo = wa > static_cast<int64_t>(s.lo) ? to_mem<kBE>(src16[-1]) : unit_at(s, wa - 1);
+    if (lane == 31) {
+      const int64_t a = wa + kSWarpVecs * 8;
+      halo = a < static_cast<int64_t>(s.hi) ? to_mem<kBE>(src16[(kSV - 1) * 32 * 8 + 8]) : unit_at(s, a);
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < kSV; k++) {
