@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "u16m_internal.h"
@@ -335,6 +336,10 @@ constexpr uint64_t kNoStart = ~0ull;
 
 __global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t count, uint32_t phase,
                                   uint64_t* __restrict__ tile_first, uint64_t nwt) {
+  // Programmatic dependent launch: let the repair grid start now; its CTAs
+  // issue their data loads and wait (griddepcontrol.wait) only before they
+  // read this table.
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint64_t s0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * kFirstPerThread;
   if (s0 >= count) return;
   const int64_t A = __ldg(offsets);
@@ -432,6 +437,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   // (kNoStart: inside a long string) scans from the next tile's first string
   // instead, which only finds whether one starts exactly at A1.
   const uint64_t wt = (wv0 - vbeg) / kSWarpVecs;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the tile table is complete and visible
   const uint64_t c0 = tile_first[wt];
   const uint64_t c1 = wt + 1 < nwt ? tile_first[wt + 1] : kNoStart;
   const uint64_t first = c0 != kNoStart ? c0 : (c1 < count ? c1 : count);
@@ -527,6 +533,14 @@ void keep_pool_memory() {
   });
 }
 
+static bool batched_pdl() {  // U16M_BATCHED_PDL=0: plain stream order (A/B)
+  static const bool v = [] {
+    const char* e = std::getenv("U16M_BATCHED_PDL");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return v;
+}
+
 cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64_t* offsets, size_t num_strings,
                                  uint16_t* out, cudaStream_t stream) {
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
@@ -557,14 +571,30 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   note_launch();
   const unsigned g = static_cast<unsigned>(ntiles_max);
   const int64_t nn = static_cast<int64_t>(n_units);
+  // Launched as a programmatic dependent of tile_first_kernel (PDL): the grid
+  // is scheduled while the pre-pass still runs.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(kSThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = batched_pdl() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const uint64_t cnt = count, nwt = nwtiles_max;
   if (in != out) {
-    batched_tile_kernel<false, 1><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nwtiles_max, nn);
+    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1>, s, offsets, cnt, ph, static_cast<const uint64_t*>(table),
+                           nwt, nn);
+  } else if (inplace_granularity() == 1) {
+    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, 1>, s, offsets, cnt, ph, static_cast<const uint64_t*>(table),
+                           nwt, nn);
   } else {
-    switch (inplace_granularity()) {
-      case 1: batched_tile_kernel<true, 1><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nwtiles_max, nn); break;
-      default: batched_tile_kernel<true, 2><<<g, kSThreads, 0, stream>>>(s, offsets, count, ph, table, nwtiles_max, nn); break;
-    }
+    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, 2>, s, offsets, cnt, ph, static_cast<const uint64_t*>(table),
+                           nwt, nn);
   }
+  if (e != cudaSuccess) return e;
   note_launch();
   e = cudaGetLastError();
   const cudaError_t f = cudaFreeAsync(table, stream);
