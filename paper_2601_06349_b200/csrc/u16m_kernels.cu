@@ -151,7 +151,10 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
   // kEmit: min(limit, total rewrites), written by tile_prefix_kernel; a tile
   // whose prefix reaches it holds nothing to emit, nor does any later tile.
   unsigned long long emit_stop = 0;
-  if constexpr (kMode == kEmit) emit_stop = *sc.count_out;
+  if constexpr (kMode == kEmit) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // launched as a dependent of tile_prefix_kernel
+    emit_stop = *sc.count_out;
+  }
   for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
     const uint64_t tile = s.tile_sel == kTilesEdges && w == 1 ? ntiles - 1 : tbase + w;
     if constexpr (kMode == kEmit) {
@@ -465,6 +468,9 @@ __global__ void __launch_bounds__(1024) tile_prefix_kernel(const uint32_t* count
                                                            unsigned long long* prefix, unsigned long long limit,
                                                            unsigned long long* count_out) {
   __shared__ unsigned long long warp_tot[32];
+  // PDL: the emit grid may launch now; this kernel waits for the counts
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long carry = 0;
   for (uint64_t base = 0; base < n; base += 1024 * kPrefixPer) {
@@ -542,10 +548,22 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   // 2) exclusive prefix + the total; 3) emit on a persistent grid that stops
   //    at the first tile ranked past the limit.
   e = launch_stream_count(in, n, nullptr, stream, counts, left, right);
+  // (2) and (3) are programmatic dependent launches (PDL): each grid is
+  // scheduled while its predecessor runs and waits (griddepcontrol.wait) only
+  // for the predecessor's results.
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
   if (e == cudaSuccess) {
-    tile_prefix_kernel<<<1, 1024, 0, stream>>>(counts, tiles, prefix, limit, count_out);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = stream;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, tile_prefix_kernel, static_cast<const uint32_t*>(counts), tiles, prefix,
+                           static_cast<unsigned long long>(limit), count_out);
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    e = cudaGetLastError();
   }
   if (e == cudaSuccess) {
     ScanArgs sc = kNoScan;
@@ -555,7 +573,14 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
     sc.offsets_out = offsets_out;
     sc.limit = limit;
     const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count_for_current_device()) * 8);
-    e = launch<kEmit, true, false>(s, kNoBatch, sc, grid, stream);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = stream;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, repair_kernel<kEmit, true, false>, s, kNoBatch, sc);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   const cudaError_t f = cudaFreeAsync(ws, stream);
   return e != cudaSuccess ? e : f;

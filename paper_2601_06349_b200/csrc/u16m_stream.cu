@@ -39,6 +39,8 @@ template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = 
           bool kNoStore = false>
 __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count,
                                                                       uint32_t* half_tile_counts) {
+  // validation: the offsets scan's prefix kernel is a programmatic dependent
+  if constexpr (kCount && kNoStore) asm volatile("griddepcontrol.launch_dependents;");
   constexpr int kSWarpVecs = 32 * kSV;
   constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
   const int lane = threadIdx.x & 31;
