@@ -29,11 +29,14 @@ def draw(rng, n):
 
 
 def test_fuzz_all_entry_points(P, cuda):
-    rng = np.random.default_rng(2026)
+    import os
+
+    # U16M_FUZZ_ITERS / U16M_FUZZ_SEED: longer or different campaigns on demand
+    rng = np.random.default_rng(int(os.environ.get("U16M_FUZZ_SEED", "2026")))
     L = P._lib.raw()
     arena = torch.zeros(1 << 21, dtype=torch.int16, device="cuda")
     arena2 = torch.zeros(1 << 21, dtype=torch.int16, device="cuda")
-    for it in range(300):
+    for it in range(int(os.environ.get("U16M_FUZZ_ITERS", "300"))):
         n = int(rng.choice([0, 1, 2, 7, 8, 9, 63, 64, 65]) if it % 4 == 0 else rng.integers(1, 900_000))
         x = draw(rng, n)
         left = int(rng.choice([-1, 0x41, 0xD801, 0xDC02]))
