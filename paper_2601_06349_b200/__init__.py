@@ -12,6 +12,8 @@ Reference-compatible names (bytes are raw UTF-16LE code units):
     fix_utf16le, fix_str, is_well_formed_utf16le, is_well_formed_str,
     unpaired_surrogate_offsets, generate_utf16le, available_kernels,
     default_kernel
+Many strings in one GPU call (batched form, no reference counterpart):
+    fix_utf16le_batch, fix_str_batch
 Device-tensor API (int16/uint16 CUDA tensors, stream-ordered, no copies):
     to_well_formed, to_well_formed_, to_well_formed_halo,
     to_well_formed_batched, count_unpaired, unpaired_offsets_device
@@ -25,8 +27,10 @@ from ._lib import (  # noqa: F401
     count_unpaired,
     default_kernel,
     fix_str,
+    fix_str_batch,
     fix_utf16_bytes,
     fix_utf16le,
+    fix_utf16le_batch,
     generate_utf16le,
     is_well_formed_str,
     is_well_formed_utf16le,
@@ -47,6 +51,8 @@ __all__ = [
     "available_kernels",
     "default_kernel",
     "fix_str",
+    "fix_str_batch",
+    "fix_utf16le_batch",
     "fix_utf16le",
     "fix_utf16_bytes",
     "to_well_formed_bytes",

@@ -274,6 +274,38 @@ def fix_str(text: str, kernel: Optional[str] = None) -> str:
     return fix_utf16le(data, kernel).decode("utf-16-le")
 
 
+_L.u16m_to_well_formed_batched_host.argtypes = [_vp, _sz, _vp, _sz, _vp]
+_L.u16m_to_well_formed_batched_host.restype = _st
+
+
+def fix_utf16le_batch(items: Sequence) -> list[bytes]:
+    """Repair many UTF-16LE byte strings with ONE GPU call (the batched form,
+    u16m_to_well_formed_batched_host): each item is repaired on its own —
+    units never pair across items — and the results come back in order.
+    For many short strings this replaces one GPU round trip per string."""
+    import numpy as np
+
+    mvs = [_check_bytes(b) for b in items]
+    if not mvs:
+        return []
+    lens = np.fromiter((m.nbytes // 2 for m in mvs), dtype=np.int64, count=len(mvs))
+    offsets = np.zeros(len(mvs) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offsets[1:])
+    n = int(offsets[-1])
+    if n == 0:
+        return [b"" for _ in mvs]
+    buf = np.frombuffer(b"".join(mvs), dtype=np.uint8).copy()   # one contiguous, writable buffer
+    _check(_L.u16m_to_well_formed_batched_host(buf.ctypes.data, n, offsets.ctypes.data, len(mvs), buf.ctypes.data))
+    raw = buf.tobytes()
+    return [raw[2 * int(a):2 * int(b)] for a, b in zip(offsets[:-1], offsets[1:])]
+
+
+def fix_str_batch(texts: Sequence[str]) -> list[str]:
+    """fix_str over many strings in one GPU call (see fix_utf16le_batch)."""
+    out = fix_utf16le_batch([t.encode("utf-16-le", "surrogatepass") for t in texts])
+    return [b.decode("utf-16-le") for b in out]
+
+
 _PyBytes_FromStringAndSize = ctypes.pythonapi.PyBytes_FromStringAndSize
 _PyBytes_FromStringAndSize.argtypes = [ctypes.c_void_p, ctypes.c_ssize_t]
 _PyBytes_FromStringAndSize.restype = ctypes.py_object

@@ -691,3 +691,20 @@ def test_other_phase_copy_all_shifts(P, cuda):
             assert (host(dst) == e).all(), (pi, po)
             rest = torch.cat([out_base[:8 + po], out_base[8 + po + n:]])
             assert bool((rest == 0x1234).all()), (pi, po)
+
+
+def test_python_batch_api(P, cuda):
+    """fix_utf16le_batch / fix_str_batch: one GPU call, per-item semantics
+    (no pairing across items), order kept, empties allowed."""
+    rng = np.random.default_rng(8)
+    items = []
+    for i in range(3000):
+        n = int(rng.choice([0, 1, 2, 3, 50, 700]))
+        items.append(rng.choice(ALPHABET, n).astype(np.uint16).tobytes())
+    items[5], items[6] = O.u16([0x41, 0xD800]).tobytes(), O.u16([0xDC00, 0x42]).tobytes()  # H | L across items
+    got = P.fix_utf16le_batch(items)
+    assert got == [O.fix_scalar(np.frombuffer(b, np.uint16)).tobytes() if b else b"" for b in items]
+    assert got[5] == O.u16([0x41, 0xFFFD]).tobytes() and got[6] == O.u16([0xFFFD, 0x42]).tobytes()
+    texts = ["ok", "", "a\ud800", "\udc00b", "\U0001F60A", "x😊y"]
+    assert P.fix_str_batch(texts) == [P.fix_str(t) for t in texts]
+    assert P.fix_utf16le_batch([]) == [] and P.fix_utf16le_batch([b"", b""]) == [b"", b""]
