@@ -147,3 +147,27 @@ def test_cli_generate_and_roundtrip(tmp_path, cuda):
     fixed = tmp_path / "fixed"
     assert run("fix", a, "-o", fixed).returncode == 0
     assert run("check", fixed).returncode == 0
+
+
+def test_cli_layout_cases(tmp_path, cuda):
+    """The in-place file-buffer path of `fix` / `check`: BOM-only and empty
+    files, --bom require, big-endian check, BE + BOM + dangling byte."""
+    inp, out = tmp_path / "in", tmp_path / "out"
+    w(inp, [0xFF, 0xFE])                               # BOM only
+    p = run("fix", inp, "-o", out)
+    assert p.returncode == 0 and p.stdout == "0 replacements\n" and r(out) == bytes([0xFF, 0xFE])
+    w(inp, [])                                         # empty file
+    assert run("fix", inp, "-o", out).returncode == 0 and r(out) == b""
+    assert run("check", inp).returncode == 0
+    w(inp, [0x41, 0x00])
+    p = run("fix", inp, "-o", out, "--bom", "require")
+    assert p.returncode != 0 and "BOM required" in p.stderr
+    w(inp, [0xFE, 0xFF, 0x00, 0x41, 0xDC, 0x00, 0x00, 0x42])   # BE, lone low at unit 1
+    p = run("check", inp)
+    assert p.returncode == 1 and p.stdout.split(":")[-1].split() == ["1"]
+    w(inp, [0xFE, 0xFF, 0xD8, 0x00, 0x00])             # BE + BOM + lone high + dangling byte
+    p = run("fix", inp, "-o", out, "--pad-final")
+    assert p.returncode == 0 and p.stdout == "2 replacements\n"
+    assert r(out) == bytes([0xFE, 0xFF, 0xFF, 0xFD, 0xFF, 0xFD])
+    p = run("fix", inp, "-o", out, "--pad-final", "--bom", "strip")
+    assert r(out) == bytes([0xFF, 0xFD, 0xFF, 0xFD])
