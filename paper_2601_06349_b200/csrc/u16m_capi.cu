@@ -1,6 +1,7 @@
-// C ABI (include/u16m.h): argument validation, stream plumbing, the host
-// staging pipeline and the multi-GPU shard driver. All compute goes through
-// the sm_100a kernels in u16m_kernels.cu — there is no CPU fallback.
+// C ABI (include/u16m.h), device-memory entry points: argument validation,
+// stream plumbing and the single-process multi-GPU shard driver. The
+// host-memory entry points live in u16m_host.cu. All compute goes through the
+// sm_100a kernels — there is no CPU fallback.
 //
 // Error behaviour mirrors the reference boundary (proj/src/driver.cpp:135-142):
 // a length/argument problem is U16M_ERR_INVALID_ARGUMENT (the reference
@@ -10,23 +11,20 @@
 // backend is missing, proj/src/bitmask_kernel.cpp:102-104).
 
 #include <cuda_runtime.h>
-#include <unistd.h>
-#include <immintrin.h>
 
 #include <algorithm>
-#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
-#include <thread>
 #include <vector>
 
 #include "../../include/u16m.h"
+#include "u16m_abi.h"
 #include "u16m_internal.h"
 
-namespace {
+namespace u16m::abi {
 
 thread_local std::string t_last_error;
 
@@ -50,8 +48,6 @@ u16m_status check_device_present() {
   return U16M_OK;
 }
 
-// Device-accessible: device or managed memory, or pinned host memory mapped
-// into the device address space.
 u16m_status check_device_ptr(const void* p, const char* name) {
   cudaPointerAttributes a;
   const cudaError_t e = cudaPointerGetAttributes(&a, p);
@@ -75,307 +71,11 @@ u16m_status check_pair(const uint16_t* in, size_t n, const uint16_t* out) {
   return U16M_OK;
 }
 
-cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace u16m::abi
 
-#define U16M_TRY(expr)                 \
-  do {                                 \
-    const u16m_status _st = (expr);    \
-    if (_st != U16M_OK) return _st;    \
-  } while (0)
+using namespace u16m::abi;
 
-// ---- host staging pipeline -------------------------------------------------
-// Three streams (H2D copy engine, compute, D2H copy engine) over a ring of
-// device chunk buffers, ordered by events: chunk c's H2D waits only for the
-// D2H that last used its buffer, so the host->device and device->host copy
-// engines both stay busy (PCIe full duplex) while the kernel runs between
-// them.
-constexpr int kRing = 8;
-constexpr size_t kChunkUnits = size_t(32) << 20;  // largest chunk: 64 MiB
-
-// Pipeline chunk in units (U16M_PIPE_CHUNK_KIB overrides; at most kChunkUnits).
-size_t pipe_chunk_units() {
-  static const size_t c = [] {
-    const char* e = std::getenv("U16M_PIPE_CHUNK_KIB");
-    size_t kib = e ? static_cast<size_t>(std::atoll(e)) : 32768;
-    size_t u = kib * 512;
-    if (u < 4096) u = 4096;
-    return u > kChunkUnits ? kChunkUnits : u;
-  }();
-  return c;
-}
-
-constexpr int kStage = 4;  // pinned bounce buffers for pageable host jobs
-
-struct HostPipe {
-  int device = -1;
-  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
-  unsigned long long* counter = nullptr;  // device replacement counter (codec jobs)
-  uint16_t* dbuf[kRing] = {};
-  cudaEvent_t loaded[kRing] = {}, repaired[kRing] = {}, drained[kRing] = {};
-  uint16_t* stage[kStage] = {};           // pinned, allocated on the first pageable job
-  cudaEvent_t staged[kStage] = {};
-};
-
-// Streaming (non-temporal) copy for the staging copies: the destination is
-// written once and read next by a DMA engine or not at all, so bypassing the
-// caches saves the read-for-ownership of every destination line.
-__attribute__((target("avx512f"))) void copy_stream_avx512(char* dst, const char* src, size_t n) {
-  size_t head = (64 - (reinterpret_cast<uintptr_t>(dst) & 63)) & 63;
-  head = std::min(head, n);
-  std::memcpy(dst, src, head);
-  dst += head, src += head, n -= head;
-  for (; n >= 256; n -= 256, dst += 256, src += 256) {
-    const __m512i a = _mm512_loadu_si512(src), b = _mm512_loadu_si512(src + 64);
-    const __m512i c = _mm512_loadu_si512(src + 128), d = _mm512_loadu_si512(src + 192);
-    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst), a);
-    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + 64), b);
-    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + 128), c);
-    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + 192), d);
-  }
-  std::memcpy(dst, src, n);
-  _mm_sfence();  // streaming stores globally visible before the copy is reported done
-}
-
-void copy_piece(char* dst, const char* src, size_t n) {
-  static const bool nt = [] {
-    const char* e = std::getenv("U16M_HOST_NT");
-    return __builtin_cpu_supports("avx512f") && !(e && std::strcmp(e, "0") == 0);
-  }();
-  if (nt) copy_stream_avx512(dst, src, n);
-  else std::memcpy(dst, src, n);
-}
-
-// Parallel host memcpy for the pageable-memory staging of the host pipeline:
-// the driver stages pageable copies through its own small bounce buffers on
-// one thread (7 GB/s measured for a 512 MiB job), so large pageable jobs are
-// copied into / out of pinned buffers by this pool instead. Worker threads
-// live for the process (the pool is never destroyed: no join at exit).
-class CopyPool {
- public:
-  static CopyPool& get() {
-    static CopyPool* pool = new CopyPool;
-    return *pool;
-  }
-  void copy(void* dst, const void* src, size_t bytes) {
-    if (getpid() != pid_) respawn();  // forked child: the workers did not survive the fork
-    if (workers_ == 0 || bytes < (size_t(1) << 20)) {
-      std::memcpy(dst, src, bytes);
-      return;
-    }
-    const size_t parts = static_cast<size_t>(workers_) + 1;
-    {
-      std::lock_guard<std::mutex> l(mu_);
-      dst_ = static_cast<char*>(dst);
-      src_ = static_cast<const char*>(src);
-      bytes_ = bytes;
-      piece_ = (bytes / parts + 4095) & ~size_t(4095);
-      pending_ = workers_;
-      ++gen_;
-    }
-    cv_.notify_all();
-    piece(workers_);  // the caller copies the last piece
-    std::unique_lock<std::mutex> l(mu_);
-    done_.wait(l, [this] { return pending_ == 0; });
-  }
-
- private:
-  CopyPool() { respawn(); }
-  void respawn() {
-    pid_ = getpid();
-    pending_ = 0;
-    const char* e = std::getenv("U16M_HOST_THREADS");
-    int t = e ? std::atoi(e) : static_cast<int>(std::thread::hardware_concurrency());
-    t = std::max(1, std::min(t, 16));
-    workers_ = t - 1;
-    const unsigned long long g = gen_;
-    for (int i = 0; i < workers_; i++) std::thread([this, i, g] { run(i, g); }).detach();
-  }
-  void piece(int i) {
-    const size_t a = std::min(bytes_, static_cast<size_t>(i) * piece_);
-    const size_t b = i == workers_ ? bytes_ : std::min(bytes_, a + piece_);
-    if (b > a) copy_piece(dst_ + a, src_ + a, b - a);
-  }
-  void run(int i, unsigned long long seen) {
-    for (;;) {
-      {
-        std::unique_lock<std::mutex> l(mu_);
-        cv_.wait(l, [&] { return gen_ != seen; });
-        seen = gen_;
-      }
-      piece(i);
-      std::lock_guard<std::mutex> l(mu_);
-      if (--pending_ == 0) done_.notify_one();
-    }
-  }
-  std::mutex mu_;
-  std::condition_variable cv_, done_;
-  int workers_ = 0, pending_ = 0;
-  pid_t pid_ = 0;
-  unsigned long long gen_ = 0;
-  char* dst_ = nullptr;
-  const char* src_ = nullptr;
-  size_t bytes_ = 0, piece_ = 0;
-};
-
-bool is_pinned(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-
-std::mutex g_pipe_mu;
-std::vector<HostPipe*> g_pipes;  // one per device, created lazily, never freed
-
-HostPipe* pipe_for(int device, u16m_status* st) {
-  for (HostPipe* p : g_pipes)
-    if (p->device == device) return p;
-  auto* p = new HostPipe;
-  p->device = device;
-  cudaError_t e = cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->comp, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&p->counter, sizeof(unsigned long long));
-  for (int i = 0; i < kRing && e == cudaSuccess; i++) {
-    e = cudaEventCreateWithFlags(&p->loaded[i], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->repaired[i], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->drained[i], cudaEventDisableTiming);
-  }
-  if (e != cudaSuccess) {
-    *st = cuda_fail(e, "host pipeline setup");
-    for (int i = 0; i < kRing; i++) {  // release what was created (null handles are skipped)
-      if (p->dbuf[i]) cudaFree(p->dbuf[i]);
-      if (p->loaded[i]) cudaEventDestroy(p->loaded[i]);
-      if (p->repaired[i]) cudaEventDestroy(p->repaired[i]);
-      if (p->drained[i]) cudaEventDestroy(p->drained[i]);
-    }
-    if (p->counter) cudaFree(p->counter);
-    if (p->h2d) cudaStreamDestroy(p->h2d);
-    if (p->comp) cudaStreamDestroy(p->comp);
-    if (p->d2h) cudaStreamDestroy(p->d2h);
-    delete p;
-    cudaGetLastError();
-    return nullptr;
-  }
-  g_pipes.push_back(p);
-  return p;
-}
-
-// Device ring slot k / pinned bounce buffer k, allocated on first use at the
-// full chunk size (a one-chunk job never pays for the other slots: cudaHostAlloc
-// of 32 MiB alone takes tens of ms).
-cudaError_t ensure_dbuf(HostPipe* p, int k) {
-  if (p->dbuf[k]) return cudaSuccess;
-  return cudaMalloc(&p->dbuf[k], pipe_chunk_units() * sizeof(uint16_t));
-}
-
-cudaError_t ensure_stage(HostPipe* p, int k) {
-  if (p->stage[k]) return cudaSuccess;
-  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p->stage[k]), pipe_chunk_units() * sizeof(uint16_t),
-                                cudaHostAllocDefault);
-  if (e == cudaSuccess && !p->staged[k]) e = cudaEventCreateWithFlags(&p->staged[k], cudaEventDisableTiming);
-  if (e != cudaSuccess && p->stage[k]) {
-    cudaFreeHost(p->stage[k]);
-    p->stage[k] = nullptr;
-  }
-  return e;
-}
-
-// Whole-buffer copies between host memory and a device buffer for the host
-// entry points that need the data resident at once (batched). Pinned host
-// memory is copied directly; pageable memory goes through two pinned bounce
-// buffers, the CopyPool filling (draining) one while the copy engine moves
-// the other. Synchronous.
-cudaError_t h2d_staged(HostPipe* p, void* dst, const void* src, size_t bytes) {
-  if (bytes == 0) return cudaSuccess;
-  if (is_pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, p->h2d) == cudaSuccess
-                                 ? cudaStreamSynchronize(p->h2d) : cudaGetLastError();
-  const size_t cb = pipe_chunk_units() * sizeof(uint16_t);
-  cudaError_t e = cudaSuccess;
-  size_t i = 0;
-  for (size_t off = 0; off < bytes && e == cudaSuccess; off += cb, i++) {
-    const int k = static_cast<int>(i % 2);
-    const size_t len = std::min(cb, bytes - off);
-    e = ensure_stage(p, k);
-    if (e == cudaSuccess && i >= 2) e = cudaEventSynchronize(p->staged[k]);  // its previous DMA is done
-    if (e != cudaSuccess) break;
-    CopyPool::get().copy(p->stage[k], static_cast<const char*>(src) + off, len);
-    e = cudaMemcpyAsync(static_cast<char*>(dst) + off, p->stage[k], len, cudaMemcpyHostToDevice, p->h2d);
-    if (e == cudaSuccess) e = cudaEventRecord(p->staged[k], p->h2d);
-  }
-  const cudaError_t f = cudaStreamSynchronize(p->h2d);
-  return e != cudaSuccess ? e : f;
-}
-
-cudaError_t d2h_staged(HostPipe* p, void* dst, const void* src, size_t bytes) {
-  if (bytes == 0) return cudaSuccess;
-  if (is_pinned(dst)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, p->d2h) == cudaSuccess
-                                 ? cudaStreamSynchronize(p->d2h) : cudaGetLastError();
-  const size_t cb = pipe_chunk_units() * sizeof(uint16_t);
-  const size_t nchunks = (bytes + cb - 1) / cb;
-  cudaError_t e = cudaSuccess;
-  auto issue = [&](size_t i) {  // DMA chunk i into bounce buffer i % 2
-    const int k = static_cast<int>(i % 2);
-    const size_t off = i * cb, len = std::min(cb, bytes - off);
-    cudaError_t r = ensure_stage(p, k);
-    if (r == cudaSuccess)
-      r = cudaMemcpyAsync(p->stage[k], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, p->d2h);
-    if (r == cudaSuccess) r = cudaEventRecord(p->staged[k], p->d2h);
-    return r;
-  };
-  e = issue(0);
-  for (size_t i = 0; i < nchunks && e == cudaSuccess; i++) {
-    const int k = static_cast<int>(i % 2);
-    if (i + 1 < nchunks) e = issue(i + 1);  // the other buffer was drained in the previous iteration
-    if (e == cudaSuccess) e = cudaEventSynchronize(p->staged[k]);
-    if (e != cudaSuccess) break;
-    const size_t off = i * cb, len = std::min(cb, bytes - off);
-    CopyPool::get().copy(static_cast<char*>(dst) + off, p->stage[k], len);
-  }
-  const cudaError_t f = cudaStreamSynchronize(p->d2h);
-  return e != cudaSuccess ? e : f;
-}
-
-// Host-path mode (U16M_HOST_MODE). Measured on the B200 box (scripts/
-// e2e_probe.py, 512 MiB, input GB/s, in place / copy; the in-place input was
-// restored by a CPU memcpy right before each call, which alone costs the H2D
-// DMA ~15 %: 45.5-46.3 in place when it is restored by DMA instead,
-// scripts/e2e_timeline_probe.py; full-duplex PCIe tops out at 46-50 each way):
-//   staged (default): H2D copy -> kernel -> D2H copy, 3 streams   39.6-41.9 / 42-46
-//   writeback: in-place jobs on pinned mapped memory stage H2D by copy engine
-//              and the kernel stores only rewritten 32-byte groups straight
-//              into host memory (no D2H copy)                          36.0 / —
-//   zerocopy: the kernel reads and writes mapped host buffers directly  36.4 / 38.5
-// Small posted PCIe writes from SMs cost more than a full-duplex DMA copy, so
-// the copy-engine pipeline stays the default. Also measured and dropped:
-// write-back at 64/128/256/512-byte groups (40.8/36.7/37.0/36.9 in place),
-// chunks of 4/8/12/16/24/64 MiB (34-40 in place; ~20 us fixed cost per
-// chunk), and a geometric ramp of the end chunks (no change, re-measured with
-// the DMA-restored input: 46.0-46.3 with and without).
-enum HostMode { kHostStaged = 0, kHostWriteback = 1, kHostZeroCopy = 2 };
-int host_mode() {
-  static const int m = [] {
-    const char* e = std::getenv("U16M_HOST_MODE");
-    if (e && std::strcmp(e, "writeback") == 0) return int(kHostWriteback);
-    if (e && std::strcmp(e, "zerocopy") == 0) return int(kHostZeroCopy);
-    return int(kHostStaged);
-  }();
-  return m;
-}
-
-// Device address of a pinned host buffer mapped into the device's address
-// space (cudaHostAlloc / cudaHostRegister memory under UVA), else nullptr.
-const uint16_t* mapped_device_ptr(const uint16_t* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return nullptr;
-  return static_cast<const uint16_t*>(a.devicePointer);
-}
+namespace {
 
 // ---- shard driver state ------------------------------------------------------
 std::mutex g_peer_mu;
@@ -553,294 +253,6 @@ u16m_status u16m_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "offsets kernels");
 }
 
-// Shared body of the host-memory entry points. byte_order < 0: plain repair
-// (units in host order); 0/1: codec-fused repair in LE/BE byte order with an
-// optional replacement count (host pointer).
-static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, int byte_order,
-                                 unsigned long long* replacements) {
-  U16M_TRY(check_pair(in, n, out));
-  if (replacements) *replacements = 0;
-  if (n == 0) return U16M_OK;
-  U16M_TRY(check_device_present());
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  std::lock_guard<std::mutex> lock(g_pipe_mu);  // one staged job per process at a time
-  u16m_status st = U16M_OK;
-  HostPipe* p = pipe_for(dev, &st);
-  if (p == nullptr) return st;
-  const bool be = byte_order == U16M_BIG_ENDIAN;
-  // Zero-copy (A/B): the stream kernel reads and writes the mapped host
-  // buffers directly over PCIe — no staging copies.
-  const uint16_t* din = mapped_device_ptr(in);
-  uint16_t* dout = const_cast<uint16_t*>(mapped_device_ptr(out));
-  if (din && dout && host_mode() == kHostZeroCopy) {
-    if (replacements) {
-      e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
-      if (e != cudaSuccess) return cuda_fail(e, "counter reset");
-    }
-    e = byte_order < 0 ? u16m::launch_repair(din, n, dout, -1, -1, nullptr, nullptr, p->comp)
-                       : u16m::launch_fix_bytes(din, n, dout, be, replacements ? p->counter : nullptr, p->comp, -1, -1);
-    if (e != cudaSuccess) return cuda_fail(e, "zero-copy repair kernel launch");
-    e = cudaStreamSynchronize(p->comp);
-    if (e == cudaSuccess && replacements)
-      e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_fail(e, "zero-copy repair");
-    return U16M_OK;
-  }
-  auto unit = [&](size_t i) -> int32_t {  // unit value of in[i] in the job's byte order
-    const uint32_t w = in[i];
-    return static_cast<int32_t>(be ? (((w & 0xFFu) << 8) | (w >> 8)) : w);
-  };
-  if (replacements) {
-    e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
-    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
-  }
-  // Pageable host memory: the copy engines cannot DMA it directly, so every
-  // chunk is copied (by the CopyPool threads) into a pinned bounce buffer,
-  // moved H2D, repaired, moved D2H back into the same bounce buffer and
-  // copied out. The host copies of chunk c+1 (in) and c+1-kStage (out)
-  // overlap the GPU work of chunk c. This replaces the driver's own
-  // single-threaded staging of pageable copies (7 GB/s on a 512 MiB job).
-  if (!is_pinned(in) || !is_pinned(out)) {
-    const size_t chunk = pipe_chunk_units();
-    CopyPool& pool = CopyPool::get();
-    const size_t nchunks = (n + chunk - 1) / chunk;
-    auto copy_out = [&](size_t c) -> cudaError_t {
-      const int k = static_cast<int>(c % kStage);
-      const cudaError_t r = cudaEventSynchronize(p->staged[k]);
-      if (r != cudaSuccess) return r;
-      const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
-      pool.copy(out + c0, p->stage[k], len * sizeof(uint16_t));
-      return cudaSuccess;
-    };
-    for (size_t c = 0; c < nchunks; c++) {
-      const int k = static_cast<int>(c % kStage);  // bounce buffer and device buffer slot
-      if (c >= static_cast<size_t>(kStage)) {
-        e = copy_out(c - kStage);  // frees slot k (its D2H is complete)
-        if (e != cudaSuccess) return cuda_fail(e, "staged D2H");
-      }
-      e = ensure_stage(p, k);
-      if (e == cudaSuccess) e = ensure_dbuf(p, k);
-      if (e != cudaSuccess) return cuda_fail(e, "staging buffers");
-      const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
-      // Halo units come from the caller's input. In place, chunks up to
-      // c - kStage have been written back by now, never c-1 or c+1 (kStage
-      // >= 2); a rewritten neighbour would be benign anyway.
-      const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
-      const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
-      pool.copy(p->stage[k], in + c0, len * sizeof(uint16_t));
-      e = cudaMemcpyAsync(p->dbuf[k], p->stage[k], len * 2, cudaMemcpyHostToDevice, p->h2d);
-      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-      cudaEventRecord(p->loaded[k], p->h2d);
-      cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-      if (byte_order < 0)
-        e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, p->comp);
-      else
-        e = u16m::launch_fix_bytes(p->dbuf[k], len, p->dbuf[k], be, replacements ? p->counter : nullptr, p->comp,
-                                   left, right);
-      if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
-      cudaEventRecord(p->repaired[k], p->comp);
-      cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
-      e = cudaMemcpyAsync(p->stage[k], p->dbuf[k], len * 2, cudaMemcpyDeviceToHost, p->d2h);
-      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
-      cudaEventRecord(p->staged[k], p->d2h);
-    }
-    for (size_t c = nchunks > static_cast<size_t>(kStage) ? nchunks - kStage : 0; c < nchunks; c++) {
-      e = copy_out(c);
-      if (e != cudaSuccess) return cuda_fail(e, "staged D2H");
-    }
-    e = cudaStreamSynchronize(p->comp);
-    if (e == cudaSuccess && replacements)
-      e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_fail(e, "host pipeline sync");
-    return U16M_OK;
-  }
-  // Write-back mode (A/B): the host buffer already holds the input, so
-  // instead of a D2H copy of every chunk the kernel stores only the 32-byte
-  // groups that hold a rewrite straight into host memory.
-  e = ensure_dbuf(p, 0);
-  if (e != cudaSuccess) return cuda_fail(e, "device chunk buffer");
-  const bool writeback = in == out && dout != nullptr && host_mode() == kHostWriteback &&
-                         ((reinterpret_cast<uintptr_t>(dout) ^ reinterpret_cast<uintptr_t>(p->dbuf[0])) & 15u) == 0;
-  size_t c = 0;
-  const size_t chunk = pipe_chunk_units();
-  for (size_t c0 = 0; c0 < n; c0 += chunk, c++) {
-    const size_t len = std::min(chunk, n - c0);
-    const int k = static_cast<int>(c % kRing);
-    // Halo units are read from the host copy at enqueue time. For in-place
-    // jobs an earlier chunk's write-back may already have rewritten in[c0-1];
-    // that is benign (a unit is only rewritten when no neighbour pairs with it).
-    const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
-    const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
-    if (c >= static_cast<size_t>(kRing)) {
-      e = cudaStreamWaitEvent(p->h2d, writeback ? p->repaired[k] : p->drained[k], 0);
-      if (e != cudaSuccess) return cuda_fail(e, "pipeline wait");
-    }
-    e = ensure_dbuf(p, k);
-    if (e != cudaSuccess) return cuda_fail(e, "device chunk buffer");
-    e = cudaMemcpyAsync(p->dbuf[k], in + c0, len * 2, cudaMemcpyHostToDevice, p->h2d);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-    cudaEventRecord(p->loaded[k], p->h2d);
-    cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-    if (writeback)
-      e = u16m::launch_stream_writeback(p->dbuf[k], len, dout + c0, left, right, be,
-                                        replacements ? p->counter : nullptr, p->comp);
-    else if (byte_order < 0)
-      e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, p->comp);
-    else
-      e = u16m::launch_fix_bytes(p->dbuf[k], len, p->dbuf[k], be, replacements ? p->counter : nullptr, p->comp,
-                                 left, right);
-    if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
-    cudaEventRecord(p->repaired[k], p->comp);
-    if (writeback) continue;
-    cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
-    e = cudaMemcpyAsync(out + c0, p->dbuf[k], len * 2, cudaMemcpyDeviceToHost, p->d2h);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
-    cudaEventRecord(p->drained[k], p->d2h);
-  }
-  e = cudaStreamSynchronize(p->d2h);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(p->h2d);
-  if (e == cudaSuccess && replacements)
-    e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return cuda_fail(e, "host pipeline sync");
-  return U16M_OK;
-}
-
-u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out) {
-  return host_pipeline(in, n, out, -1, nullptr);
-}
-
-u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out, int byte_order,
-                                      unsigned long long* replacements) {
-  if (byte_order != U16M_LITTLE_ENDIAN && byte_order != U16M_BIG_ENDIAN)
-    return fail(U16M_ERR_INVALID_ARGUMENT, "byte_order must be U16M_LITTLE_ENDIAN or U16M_BIG_ENDIAN");
-  return host_pipeline(static_cast<const uint16_t*>(in), n_units, static_cast<uint16_t*>(out), byte_order,
-                       replacements);
-}
-
-u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units, const int64_t* offsets,
-                                             size_t num_strings, uint16_t* out) {
-  if (offsets == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "offsets is null");
-  U16M_TRY(check_pair(in, n_units, out));
-  if (num_strings == 0 || n_units == 0) {
-    if (out != in && n_units) std::memcpy(out, in, n_units * sizeof(uint16_t));
-    return U16M_OK;
-  }
-  for (size_t s = 0; s < num_strings; s++)
-    if (offsets[s] < 0 || offsets[s + 1] < offsets[s] || static_cast<size_t>(offsets[s + 1]) > n_units)
-      return fail(U16M_ERR_INVALID_ARGUMENT, "offsets must be non-decreasing within the buffer");
-  U16M_TRY(check_device_present());
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  std::lock_guard<std::mutex> lock(g_pipe_mu);
-  u16m_status st = U16M_OK;
-  HostPipe* p = pipe_for(dev, &st);
-  if (p == nullptr) return st;
-  u16m::keep_pool_memory();
-  const size_t data_bytes = n_units * sizeof(uint16_t), off_bytes = (num_strings + 1) * sizeof(int64_t);
-  const size_t off_at = (data_bytes + 15) / 16 * 16;
-  void* ws = nullptr;
-  e = cudaMallocAsync(&ws, off_at + off_bytes, p->comp);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
-  if (e != cudaSuccess) return cuda_fail(e, "device buffer");
-  auto* d_data = static_cast<uint16_t*>(ws);
-  auto* d_off = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + off_at);
-  e = h2d_staged(p, d_data, in, data_bytes);
-  if (e == cudaSuccess) e = h2d_staged(p, d_off, offsets, off_bytes);
-  if (e == cudaSuccess) {
-    const cudaError_t k = u16m::launch_batched_tiles(d_data, n_units, d_off, num_strings, d_data, p->comp);
-    e = k != cudaSuccess ? k : cudaStreamSynchronize(p->comp);
-  }
-  if (e == cudaSuccess) e = d2h_staged(p, out, d_data, data_bytes);
-  cudaFreeAsync(ws, p->comp);
-  const cudaError_t f = cudaStreamSynchronize(p->comp);
-  if (e != cudaSuccess) return cuda_fail(e, "batched host repair");
-  if (f != cudaSuccess) return cuda_fail(f, "batched host repair");
-  return U16M_OK;
-}
-
-u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,
-                                       unsigned long long* offsets_out, size_t* count_out) {
-  if (count_out == nullptr || (limit > 0 && offsets_out == nullptr))
-    return fail(U16M_ERR_INVALID_ARGUMENT, "null output");
-  *count_out = 0;
-  if (n == 0 || limit == 0) return U16M_OK;
-  if (in == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "null buffer with n > 0");
-  if (reinterpret_cast<uintptr_t>(in) & 1u) return fail(U16M_ERR_MISALIGNED, "in not 2-byte aligned");
-  U16M_TRY(check_device_present());
-  if (limit > n) limit = n;
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  std::lock_guard<std::mutex> lock(g_pipe_mu);
-  u16m_status st = U16M_OK;
-  HostPipe* p = pipe_for(dev, &st);
-  if (p == nullptr) return st;
-  // Chunked, read-only scan: chunk c+1 moves H2D (straight from pinned memory,
-  // or through a pinned bounce buffer filled by the CopyPool) while chunk c
-  // is scanned with its neighbours' units as halos; the scan stops at the
-  // first chunk that completes `limit` offsets (the CLI check asks for 10,
-  // is_well_formed for 1), so an ill-formed buffer is rarely read to its end.
-  const bool pinned = is_pinned(in);
-  const size_t chunk = pipe_chunk_units();
-
-  const size_t cap = std::min(limit, chunk);
-  void* ws = nullptr;
-  u16m::keep_pool_memory();
-  e = cudaMallocAsync(&ws, cap * sizeof(unsigned long long) + 64, p->comp);
-  if (e != cudaSuccess) return cuda_fail(e, "workspace");
-  auto* d_off = static_cast<unsigned long long*>(ws);
-  auto* d_cnt = d_off + cap;
-  const size_t nchunks = (n + chunk - 1) / chunk;
-  auto load = [&](size_t c) -> cudaError_t {  // H2D of chunk c into device slot c % 2
-    const int k = static_cast<int>(c % 2);
-    cudaError_t r = ensure_dbuf(p, k);
-    if (r == cudaSuccess && !pinned) r = ensure_stage(p, k);
-    if (r != cudaSuccess) return r;
-    const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
-    const uint16_t* src = in + c0;
-    if (!pinned) {
-      CopyPool::get().copy(p->stage[k], src, len * sizeof(uint16_t));
-      src = p->stage[k];
-    }
-    r = cudaMemcpyAsync(p->dbuf[k], src, len * 2, cudaMemcpyHostToDevice, p->h2d);
-    if (r == cudaSuccess) cudaEventRecord(p->loaded[k], p->h2d);
-    return r;
-  };
-  size_t found = 0;
-  e = load(0);
-  for (size_t c = 0; c < nchunks && e == cudaSuccess; c++) {
-    const int k = static_cast<int>(c % 2);
-    const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
-    // the next chunk's slot was last read by chunk c-1's scan, finished below
-    if (c + 1 < nchunks) e = load(c + 1);
-    if (e != cudaSuccess) break;
-    cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-    const int32_t left = c0 > 0 ? in[c0 - 1] : -1;
-    const int32_t right = c0 + len < n ? in[c0 + len] : -1;
-    e = u16m::launch_unpaired_offsets(p->dbuf[k], len, std::min(limit - found, cap), d_off, d_cnt, p->comp,
-                                      left, right);
-    if (e != cudaSuccess) break;
-    unsigned long long cnt = 0;
-    e = cudaMemcpyAsync(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, p->comp);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
-    if (e == cudaSuccess && cnt) e = cudaMemcpy(offsets_out + found, d_off, cnt * 8, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) break;
-    for (size_t i = 0; i < cnt; i++) offsets_out[found + i] += c0;  // chunk-relative -> buffer offsets
-    found += cnt;
-    if (found >= limit) break;
-  }
-  const cudaError_t f = cudaStreamSynchronize(p->h2d);  // a prefetched chunk may still read `in`
-  cudaFreeAsync(ws, p->comp);
-  cudaStreamSynchronize(p->comp);
-  if (e != cudaSuccess) return cuda_fail(e, "unpaired offsets");
-  if (f != cudaSuccess) return cuda_fail(f, "unpaired offsets");
-  *count_out = found;
-  return U16M_OK;
-}
 
 u16m_status u16m_to_well_formed_sharded(int num_shards, const int* device_ids,
                                         const uint16_t* const* shard_in, const size_t* shard_len,
