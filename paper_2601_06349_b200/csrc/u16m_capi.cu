@@ -218,8 +218,7 @@ u16m_status u16m_to_well_formed_batched_n(const uint16_t* in, size_t n_units, co
   U16M_TRY(check_device_ptr(in, "in"));
   if (out != in) U16M_TRY(check_device_ptr(out, "out"));
   U16M_TRY(check_device_ptr(offsets, "offsets"));
-  const bool same16 = ((reinterpret_cast<uintptr_t>(in) ^ reinterpret_cast<uintptr_t>(out)) & 15u) == 0;
-  const cudaError_t e = same16 && u16m::batched_tiles_enabled()
+  const cudaError_t e = u16m::batched_tiles_enabled()  // any in/out phase (shifted stores when they differ)
                             ? u16m::launch_batched_tiles(in, n_units, offsets, num_strings, out, as_stream(stream))
                             : u16m::launch_batched(in, offsets, num_strings, out, as_stream(stream));
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "batched repair kernel launch");

@@ -384,11 +384,15 @@ __device__ __forceinline__ void scan_window(int64_t p, int64_t A0, int64_t A1, i
   }
 }
 
-template <bool kInPlace, int kGran>
+// kShift > 0 (copy only): `out` has a different 16-byte phase than `in`;
+// s.out is out's 16-byte-aligned base, s.out_units the caller's out pointer,
+// and vectors are stored shifted as in stream_shift_kernel (q: vector offset).
+template <bool kInPlace, int kGran, int kShift = 0>
 __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, const int64_t* __restrict__ offsets,
                                                                     uint64_t count, uint32_t phase,
                                                                     const uint64_t* __restrict__ tile_first,
-                                                                    uint64_t nwt, int64_t n_units) {
+                                                                    uint64_t nwt, int64_t n_units, int64_t q) {
+  static_assert(kShift == 0 || !kInPlace, "in place is always the same phase");
   const int lane = threadIdx.x & 31;
   {
     // Clamp to the caller's buffer: offsets beyond it are a contract error,
@@ -398,7 +402,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
     A = A < B ? A : B;
     s.lo = static_cast<uint64_t>(A) + phase;
     s.hi = static_cast<uint64_t>(B) + phase;
-    s.out_units = reinterpret_cast<uint16_t*>(s.out) + s.lo;
+    s.out_units = kShift ? s.out_units + A : reinterpret_cast<uint16_t*>(s.out) + s.lo;
   }
   if (s.hi <= s.lo) return;
   const uint64_t vbeg = s.lo / 8;
@@ -472,6 +476,7 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   for (int k = 0; k < kSV; k++) need |= (static_cast<uint32_t>(M >> (8 * k)) & 0xFFu) ? (1u << k) : 0u;
   need = __reduce_or_sync(kFull, need);
 
+  uint4 shift_carry = make_uint4(0, 0, 0, 0);  // kShift: lane 31's repaired vector k-1
   Flags cur = classify8(v[0]);
   uint32_t hp_carry = hflag_hi(halo);
   const uint32_t halo_l = lflag_lo(halo);
@@ -501,7 +506,30 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
       bad8(cur, hp, ln, B0, B1);
     const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
     const uint64_t vi = v0 + k * 32;
-    if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
+    if constexpr (kShift > 0) {
+      const uint4 r = blend(v[k], B0, B1);
+      if (interior) {
+        uint4 prev = shfl4(r, 0, true);
+        if (lane == 0) prev = shift_carry;
+        shift_carry = shfl4(r, 31, false);
+        if (k == 0 && lane == 0) {  // head of the vector straddling the warp tile start
+#pragma unroll
+          for (int j = 0; j < 8 - kShift; j++) s.out_units[vi * 8 + j - s.lo] = static_cast<uint16_t>(get_unit(r, j));
+        } else {
+          st_stream(s.out + static_cast<int64_t>(vi) + q, combine_units<kShift>(prev, r));
+        }
+        if (k == kSV - 1 && lane == 31) {
+#pragma unroll
+          for (int j = 8 - kShift; j < 8; j++) s.out_units[vi * 8 + j - s.lo] = static_cast<uint16_t>(get_unit(r, j));
+        }
+      } else if (vi < vend) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const uint64_t a = vi * 8 + j;
+          if (a >= s.lo && a < s.hi) s.out_units[a - s.lo] = static_cast<uint16_t>(get_unit(r, j));
+        }
+      }
+    } else if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
       if (store) st_stream(s.out + vi, blend(v[k], B0, B1));
     } else if (store && vi < vend) {
       const uint4 r = blend(v[k], B0, B1);
@@ -586,15 +614,32 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const uint64_t cnt = count, nwt = nwtiles_max;
-  if (in != out) {
-    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1>, s, offsets, cnt, ph, static_cast<const uint64_t*>(table),
-                           nwt, nn);
+  const uint64_t* tab = table;
+  const int64_t q0 = 0;
+  const int64_t po = static_cast<int64_t>((oa & 15u) / 2);
+  const int64_t delta = po - static_cast<int64_t>(ph);
+  const int sh = static_cast<int>(((delta % 8) + 8) % 8);
+  if (sh != 0) {
+    // out at a different 16-byte phase: shifted vector stores (copy only)
+    Span t = s;
+    t.out = reinterpret_cast<uint4*>(oa - 2 * po);
+    t.out_units = out;
+    const int64_t q = (delta - sh) / 8;
+    switch (sh) {
+      case 1: e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1, 1>, t, offsets, cnt, ph, tab, nwt, nn, q); break;
+      case 2: e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1, 2>, t, offsets, cnt, ph, tab, nwt, nn, q); break;
+      case 3: e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1, 3>, t, offsets, cnt, ph, tab, nwt, nn, q); break;
+      case 4: e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1, 4>, t, offsets, cnt, ph, tab, nwt, nn, q); break;
+      case 5: e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1, 5>, t, offsets, cnt, ph, tab, nwt, nn, q); break;
+      case 6: e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1, 6>, t, offsets, cnt, ph, tab, nwt, nn, q); break;
+      default: e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1, 7>, t, offsets, cnt, ph, tab, nwt, nn, q); break;
+    }
+  } else if (in != out) {
+    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1>, s, offsets, cnt, ph, tab, nwt, nn, q0);
   } else if (inplace_granularity() == 1) {
-    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, 1>, s, offsets, cnt, ph, static_cast<const uint64_t*>(table),
-                           nwt, nn);
+    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, 1>, s, offsets, cnt, ph, tab, nwt, nn, q0);
   } else {
-    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, 2>, s, offsets, cnt, ph, static_cast<const uint64_t*>(table),
-                           nwt, nn);
+    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, 2>, s, offsets, cnt, ph, tab, nwt, nn, q0);
   }
   if (e != cudaSuccess) return e;
   note_launch();

@@ -533,8 +533,8 @@ def test_batched_entry_without_length(P, cuda, golden):
 
 
 def test_batched_other_phase_and_copy(P, cuda):
-    """Batched copy into an output whose 16-byte phase differs from the input
-    (general-kernel path) and into an aligned output (tile kernel)."""
+    """Batched copy into an output at every 16-byte phase relative to the
+    input (shifted stores in the tile kernel) and into an aligned output."""
     rng = np.random.default_rng(41)
     lens = rng.choice([0, 1, 2, 3, 17, 300, 4095, 20000], 2000)
     offsets = np.zeros(lens.size + 1, np.int64)
@@ -544,7 +544,7 @@ def test_batched_other_phase_and_copy(P, cuda):
     e = O.fix_batched(data, offsets)
     t = dev(data)
     o = torch.from_numpy(offsets).cuda()
-    for shift in (0, 1, 3, 8):
+    for shift in range(9):
         big = torch.full((t.numel() + 16,), 0x1234, dtype=torch.int16, device="cuda")
         out = big[shift:shift + t.numel()]
         out.copy_(t)
