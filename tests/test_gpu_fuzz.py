@@ -75,3 +75,10 @@ def test_fuzz_all_entry_points(P, cuda):
         eb = O.fix_batched(x, offs)
         got = host(P.to_well_formed_batched(dev(x), torch.from_numpy(offs).cuda()))
         assert (got == eb).all(), ("batched", it, n)
+        # batched from the phase-pi source into a phase-po output (shifted stores when they differ)
+        if n:
+            src.copy_(dev(x))
+            bo = arena2[po:po + n]
+            bo.copy_(src)
+            P.to_well_formed_batched(src, torch.from_numpy(offs).cuda(), out=bo)
+            assert (host(bo) == eb).all(), ("batched phases", it, n, pi, po)
