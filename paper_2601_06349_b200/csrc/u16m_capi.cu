@@ -197,14 +197,19 @@ u16m_status u16m_fix_utf16_bytes(const void* in, size_t n_units, void* out, int 
   auto* o = static_cast<uint16_t*>(out);
   U16M_TRY(check_pair(i, n_units, o));
   if (n_units == 0) return U16M_OK;
-  if (i != o && ((reinterpret_cast<uintptr_t>(i) ^ reinterpret_cast<uintptr_t>(o)) & 15u))
-    return fail(U16M_ERR_MISALIGNED, "byte-order-aware repair needs in/out with the same 16-byte phase");
   U16M_TRY(check_device_present());
   U16M_TRY(check_device_ptr(in, "in"));
   if (o != i) U16M_TRY(check_device_ptr(out, "out"));
   if (replacements) U16M_TRY(check_device_ptr(replacements, "replacements"));
-  const cudaError_t e = u16m::launch_fix_bytes(in, n_units, out, byte_order == U16M_BIG_ENDIAN, replacements,
-                                              as_stream(stream), -1, -1);
+  const bool be = byte_order == U16M_BIG_ENDIAN;
+  if (i != o && ((reinterpret_cast<uintptr_t>(i) ^ reinterpret_cast<uintptr_t>(o)) & 15u)) {
+    // out at another 16-byte phase (rare for byte streams): copy the bytes
+    // across, then repair them in place — two passes, any alignment.
+    cudaError_t e = cudaMemcpyAsync(o, i, n_units * sizeof(uint16_t), cudaMemcpyDeviceToDevice, as_stream(stream));
+    if (e == cudaSuccess) e = u16m::launch_fix_bytes(o, n_units, o, be, replacements, as_stream(stream), -1, -1);
+    return e == cudaSuccess ? U16M_OK : cuda_fail(e, "codec repair (other-phase output)");
+  }
+  const cudaError_t e = u16m::launch_fix_bytes(in, n_units, out, be, replacements, as_stream(stream), -1, -1);
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "codec repair kernel launch");
 }
 

@@ -171,3 +171,20 @@ def test_cli_layout_cases(tmp_path, cuda):
     assert r(out) == bytes([0xFE, 0xFF, 0xFF, 0xFD, 0xFF, 0xFD])
     p = run("fix", inp, "-o", out, "--pad-final", "--bom", "strip")
     assert r(out) == bytes([0xFF, 0xFD, 0xFF, 0xFD])
+
+
+def test_codec_other_phase_output(cuda):
+    """Byte-order-fused repair into an output at another 16-byte phase (copy,
+    then in place) — any alignment works, with the right replacement count."""
+    x = np.frombuffer(P.generate_utf16le(100_003, 0.05, 0.02, 3), np.uint16)
+    e = O.fix_scalar(x)
+    for big in (False, True):
+        raw = (x.astype(">u2") if big else x).view(np.uint16)
+        t = torch.from_numpy(raw.view(np.int16).copy()).cuda()
+        for po in (1, 3, 8):
+            base = torch.zeros(x.size + 16, dtype=torch.int16, device="cuda")
+            out = base[po:po + x.size]
+            got, cnt = P.to_well_formed_bytes(t, out=out, big_endian=big, count=True)
+            h = got.cpu().numpy().view(np.uint16)
+            h = h.view(">u2").astype(np.uint16) if big else h
+            assert (h == e).all() and cnt == int((x != e).sum()), (big, po)
