@@ -112,6 +112,17 @@ u16m_status u16m_to_well_formed_sharded(int num_shards, const int* device_ids,
  * streams). Synchronous. Pinned host memory gets full-duplex DMA. */
 u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out);
 
+/* Host-memory form over several GPUs (north star item 5 for host-resident
+ * data; behind utf16mend::to_well_formed on host spans, which replaces
+ * proj/src/driver.cpp:135-147): the buffer is cut into contiguous ranges, one
+ * per device, each streamed through that device's own pipeline and PCIe link
+ * concurrently (one host thread per extra device); the halo unit at each
+ * range edge is read from the caller's input. num_devices = 0 (device_ids
+ * NULL) = every visible device. Ranges are at least 32 Mi units, so small
+ * jobs use fewer devices. Ids may repeat. Synchronous; in == out or disjoint. */
+u16m_status u16m_to_well_formed_host_multi(const uint16_t* in, size_t n, uint16_t* out, int num_devices,
+                                           const int* device_ids);
+
 /* §8(f) row 1 — validation. Device pointers. `count_out` (device, uint64) gets
  * the number of units repair would rewrite; is_well_formed <=> count == 0.
  * Async; the caller reads count_out after synchronising `stream`. */
@@ -153,6 +164,20 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
  * num_strings + 1 non-decreasing entries within [0, n_units]. Synchronous. */
 u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units, const int64_t* offsets,
                                              size_t num_strings, uint16_t* out);
+
+/* The reference's kernel-selection names (proj/src/driver.cpp:15-108):
+ * available_kernels() comma-joined, and select_kernel() (honours
+ * UTF16MEND_KERNEL, warning on bad values as the reference does). Every name
+ * is served by the one sm_100a path. Writes a NUL-terminated string of at most
+ * cap bytes; returns the full length. (Python available_kernels /
+ * default_kernel, proj/bindings/module.cpp:93-104.) */
+int u16m_kernel_names(char* buf, size_t cap);
+int u16m_default_kernel_name(char* buf, size_t cap);
+/* select_kernel(parse_kernel_id(name)) (name NULL = no override): writes the
+ * chosen name; an unknown name or an override the host does not support
+ * returns U16M_ERR_INVALID_ARGUMENT with the reference's message in
+ * u16m_last_error() (proj/src/driver.cpp:71-86, proj/bindings/module.cpp:42-47). */
+u16m_status u16m_select_kernel(const char* name, char* buf, size_t cap);
 
 const char* u16m_status_string(u16m_status status);
 const char* u16m_last_error(void);

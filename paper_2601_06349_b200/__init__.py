@@ -24,6 +24,7 @@ from ._lib import (  # noqa: F401
     U16MError,
     api_version,
     available_kernels,
+    backend,
     count_unpaired,
     default_kernel,
     fix_str,
@@ -49,6 +50,7 @@ from ._lib import (  # noqa: F401
 
 __all__ = [
     "available_kernels",
+    "backend",
     "default_kernel",
     "fix_str",
     "fix_str_batch",

@@ -67,10 +67,14 @@ for _f in ("u16m_to_well_formed", "u16m_to_well_formed_in_place", "u16m_to_well_
 
 OK, INVALID, ALIAS, NOT_DEVICE, CUDA, MISALIGNED, NO_DEVICE = range(7)
 
-# Reference kernel names (proj/src/driver.cpp:25-37) are accepted for source
-# compatibility and all served by the one sm_100a path.
-_KERNEL_NAMES = {"scalar", "generic", "generic4", "generic8", "generic16", "generic32", "bitmask",
-                 "bitmask-emulated", "bytesplit", "bytesplit-emulated", "cuda", "cuda-sm100a"}
+_L.u16m_kernel_names.argtypes = [ctypes.c_char_p, _sz]
+_L.u16m_kernel_names.restype = ctypes.c_int
+_L.u16m_default_kernel_name.argtypes = [ctypes.c_char_p, _sz]
+_L.u16m_default_kernel_name.restype = ctypes.c_int
+_L.u16m_select_kernel.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _sz]
+_L.u16m_select_kernel.restype = _st
+_L.u16m_to_well_formed_host_multi.argtypes = [_u16p, _sz, _u16p, ctypes.c_int, _vp]
+_L.u16m_to_well_formed_host_multi.restype = _st
 
 
 class U16MError(RuntimeError):
@@ -241,8 +245,15 @@ def unpaired_offsets_device(x: torch.Tensor, limit: Optional[int] = None, stream
 
 # ---- reference-compatible bytes API (proj/bindings/module.cpp) ---------------
 def _kernel_from_name(kernel: Optional[str]) -> None:
-    if kernel is not None and kernel not in _KERNEL_NAMES:
-        raise ValueError(f"unknown kernel '{kernel}'")
+    """The reference's kernel validation (module.cpp:42-47 + driver.cpp:71-86):
+    an unknown name, or an override this host does not support, raises
+    ValueError with the reference's message. Every kernel id is served by the
+    one sm_100a path."""
+    if kernel is None:
+        return
+    buf = ctypes.create_string_buffer(64)
+    if _L.u16m_select_kernel(kernel.encode(), buf, 64) != OK:
+        raise ValueError((_L.u16m_last_error() or b"").decode())
 
 
 def _check_bytes(data) -> memoryview:
@@ -255,7 +266,8 @@ def _check_bytes(data) -> memoryview:
 def fix_utf16le(data, kernel: Optional[str] = None) -> bytes:
     """Return `data` (raw UTF-16LE code units) with every unpaired surrogate
     replaced by U+FFFD (module.cpp:54-64). Host memory is staged through the
-    GPU by u16m_to_well_formed_host."""
+    visible GPUs by u16m_to_well_formed_host_multi (the call behind the C++
+    to_well_formed on host spans)."""
     mv = _check_bytes(data)
     _kernel_from_name(kernel)
     n = mv.nbytes // 2
@@ -263,7 +275,7 @@ def fix_utf16le(data, kernel: Optional[str] = None) -> bytes:
         return b""
     src = _host_ptr(mv)                         # read in place, no Python-side copy
     out, addr = _new_bytes(mv.nbytes)
-    _check(_L.u16m_to_well_formed_host(src.ctypes.data, n, addr))
+    _check(_L.u16m_to_well_formed_host_multi(src.ctypes.data, n, addr, 0, None))
     return out
 
 
@@ -410,11 +422,23 @@ def to_well_formed_bytes(x: torch.Tensor, out: Optional[torch.Tensor] = None, bi
 
 
 def available_kernels() -> list[str]:
-    """Names of every repair kernel selectable on this host (module.cpp:95-102)."""
-    return ["cuda-sm100a"]
+    """Names of every repair kernel selectable on this host (module.cpp:95-102),
+    the reference's list; all of them run the one sm_100a path."""
+    buf = ctypes.create_string_buffer(512)
+    _L.u16m_kernel_names(buf, 512)
+    return buf.value.decode().split(",")
 
 
 def default_kernel() -> str:
+    """Kernel the driver picks on this host (honours UTF16MEND_KERNEL), as the
+    reference names it (module.cpp:104-106)."""
+    buf = ctypes.create_string_buffer(64)
+    _L.u16m_default_kernel_name(buf, 64)
+    return buf.value.decode()
+
+
+def backend() -> str:
+    """The implementation every kernel name runs on."""
     return "cuda-sm100a"
 
 

@@ -56,6 +56,7 @@ struct HostPipe {
   cudaEvent_t loaded[kRing] = {}, repaired[kRing] = {}, drained[kRing] = {};
   uint16_t* stage[kStage] = {};           // pinned, allocated on the first pageable job
   cudaEvent_t staged[kStage] = {};
+  std::mutex mu;                          // one job per device pipeline at a time
 };
 
 // Streaming (non-temporal) copy for the staging copies: the destination is
@@ -99,8 +100,13 @@ class CopyPool {
     return *pool;
   }
   void copy(void* dst, const void* src, size_t bytes) {
+    if (bytes < (size_t(1) << 20)) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> job(job_mu_);  // device threads of a multi-GPU job share the pool
     if (getpid() != pid_) respawn();  // forked child: the workers did not survive the fork
-    if (workers_ == 0 || bytes < (size_t(1) << 20)) {
+    if (workers_ == 0) {
       std::memcpy(dst, src, bytes);
       return;
     }
@@ -149,7 +155,7 @@ class CopyPool {
       if (--pending_ == 0) done_.notify_one();
     }
   }
-  std::mutex mu_;
+  std::mutex job_mu_, mu_;
   std::condition_variable cv_, done_;
   int workers_ = 0, pending_ = 0;
   pid_t pid_ = 0;
@@ -168,10 +174,13 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-std::mutex g_pipe_mu;
+std::mutex g_pipes_mu;
 std::vector<HostPipe*> g_pipes;  // one per device, created lazily, never freed
 
+// The device's pipeline (created on first use on the calling thread, which
+// must have made `device` current). Jobs lock HostPipe::mu.
 HostPipe* pipe_for(int device, u16m_status* st) {
+  std::lock_guard<std::mutex> lock(g_pipes_mu);
   for (HostPipe* p : g_pipes)
     if (p->device == device) return p;
   auto* p = new HostPipe;
@@ -280,92 +289,41 @@ cudaError_t d2h_staged(HostPipe* p, void* dst, const void* src, size_t bytes) {
   return e != cudaSuccess ? e : f;
 }
 
-// Host-path mode (U16M_HOST_MODE). Measured on the B200 box (scripts/
-// e2e_probe.py, 512 MiB, input GB/s, in place / copy; the in-place input was
-// restored by a CPU memcpy right before each call, which alone costs the H2D
-// DMA ~15 %: 45.5-46.3 in place when it is restored by DMA instead,
-// scripts/e2e_timeline_probe.py; full-duplex PCIe tops out at 46-50 each way):
-//   staged (default): H2D copy -> kernel -> D2H copy, 3 streams   39.6-41.9 / 42-46
-//   writeback: in-place jobs on pinned mapped memory stage H2D by copy engine
-//              and the kernel stores only rewritten 32-byte groups straight
-//              into host memory (no D2H copy)                          36.0 / —
-//   zerocopy: the kernel reads and writes mapped host buffers directly  36.4 / 38.5
-// Small posted PCIe writes from SMs cost more than a full-duplex DMA copy, so
-// the copy-engine pipeline stays the default. Also measured and dropped:
-// write-back at 64/128/256/512-byte groups (40.8/36.7/37.0/36.9 in place),
-// chunks of 4/8/12/16/24/64 MiB (34-40 in place; ~20 us fixed cost per
-// chunk), and a geometric ramp of the end chunks (no change, re-measured with
-// the DMA-restored input: 46.0-46.3 with and without).
-enum HostMode { kHostStaged = 0, kHostWriteback = 1, kHostZeroCopy = 2 };
-int host_mode() {
-  static const int m = [] {
-    const char* e = std::getenv("U16M_HOST_MODE");
-    if (e && std::strcmp(e, "writeback") == 0) return int(kHostWriteback);
-    if (e && std::strcmp(e, "zerocopy") == 0) return int(kHostZeroCopy);
-    return int(kHostStaged);
-  }();
-  return m;
-}
+// Host jobs run the staged copy-engine pipeline: H2D copy -> repair kernel ->
+// D2H copy on 3 streams over a ring of device chunks. Measured on the B200
+// box and dropped (round 1, scripts/e2e_probe.py, 512 MiB in place / copy,
+// input GB/s; full-duplex PCIe tops out at 46-50 each way): the kernel
+// storing only rewritten 32-byte groups straight into mapped host memory
+// (36.0 / -), and the kernel reading and writing mapped host buffers directly
+// (36.4 / 38.5) — small posted PCIe writes from SMs cost more than a
+// full-duplex DMA copy. Also dropped: write-back at 64-512-byte groups
+// (36.7-40.8), chunks of 4-64 MiB (34-40 in place; ~20 us fixed cost per
+// chunk), a geometric ramp of the end chunks (no change).
 
-// Device address of a pinned host buffer mapped into the device's address
-// space (cudaHostAlloc / cudaHostRegister memory under UVA), else nullptr.
-const uint16_t* mapped_device_ptr(const uint16_t* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return nullptr;
-  return static_cast<const uint16_t*>(a.devicePointer);
-}
-
-}  // namespace
-
-extern "C" {
-
-// Shared body of the host-memory entry points. byte_order < 0: plain repair
-// (units in host order); 0/1: codec-fused repair in LE/BE byte order with an
-// optional replacement count (host pointer).
-static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, int byte_order,
-                                 unsigned long long* replacements) {
-  U16M_TRY(check_pair(in, n, out));
-  if (replacements) *replacements = 0;
-  if (n == 0) return U16M_OK;
-  U16M_TRY(check_device_present());
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  std::lock_guard<std::mutex> lock(g_pipe_mu);  // one staged job per process at a time
-  u16m_status st = U16M_OK;
-  HostPipe* p = pipe_for(dev, &st);
-  if (p == nullptr) return st;
+// One host job's share on one device: units [a, b) of the caller's buffers
+// (`in`/`out` hold n units), halo units read from the caller's input at
+// a-1 and b (-1 at the buffer's ends). The calling thread must have made
+// p->device current and hold p->mu. Device replacement counts (codec jobs)
+// accumulate in p->counter, which the caller reset.
+u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out, size_t a, size_t b,
+                       int byte_order, bool count) {
+  cudaError_t e = cudaSuccess;
   const bool be = byte_order == U16M_BIG_ENDIAN;
-  // Zero-copy (A/B): the stream kernel reads and writes the mapped host
-  // buffers directly over PCIe — no staging copies.
-  const uint16_t* din = mapped_device_ptr(in);
-  uint16_t* dout = const_cast<uint16_t*>(mapped_device_ptr(out));
-  if (din && dout && host_mode() == kHostZeroCopy) {
-    if (replacements) {
-      e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
-      if (e != cudaSuccess) return cuda_fail(e, "counter reset");
-    }
-    e = byte_order < 0 ? u16m::launch_repair(din, n, dout, -1, -1, nullptr, nullptr, p->comp)
-                       : u16m::launch_fix_bytes(din, n, dout, be, replacements ? p->counter : nullptr, p->comp, -1, -1);
-    if (e != cudaSuccess) return cuda_fail(e, "zero-copy repair kernel launch");
-    e = cudaStreamSynchronize(p->comp);
-    if (e == cudaSuccess && replacements)
-      e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_fail(e, "zero-copy repair");
-    return U16M_OK;
-  }
   auto unit = [&](size_t i) -> int32_t {  // unit value of in[i] in the job's byte order
     const uint32_t w = in[i];
     return static_cast<int32_t>(be ? (((w & 0xFFu) << 8) | (w >> 8)) : w);
   };
-  if (replacements) {
-    e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
-    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
-  }
+  auto repair = [&](uint16_t* d, size_t c0, size_t len) {
+    // Halo units come from the caller's input at enqueue time. In place, a
+    // neighbouring chunk (or another device's range) may already have been
+    // written back; a rewritten neighbour is benign (a unit is only rewritten
+    // when no neighbour pairs with it).
+    const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
+    const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
+    return byte_order < 0 ? u16m::launch_repair(d, len, d, left, right, nullptr, nullptr, p->comp)
+                          : u16m::launch_fix_bytes(d, len, d, be, count ? p->counter : nullptr, p->comp, left, right);
+  };
+  const size_t chunk = pipe_chunk_units();
   // Pageable host memory: the copy engines cannot DMA it directly, so every
   // chunk is copied (by the CopyPool threads) into a pinned bounce buffer,
   // moved H2D, repaired, moved D2H back into the same bounce buffer and
@@ -373,14 +331,13 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
   // overlap the GPU work of chunk c. This replaces the driver's own
   // single-threaded staging of pageable copies (7 GB/s on a 512 MiB job).
   if (!is_pinned(in) || !is_pinned(out)) {
-    const size_t chunk = pipe_chunk_units();
     CopyPool& pool = CopyPool::get();
-    const size_t nchunks = (n + chunk - 1) / chunk;
+    const size_t nchunks = (b - a + chunk - 1) / chunk;
     auto copy_out = [&](size_t c) -> cudaError_t {
       const int k = static_cast<int>(c % kStage);
       const cudaError_t r = cudaEventSynchronize(p->staged[k]);
       if (r != cudaSuccess) return r;
-      const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
+      const size_t c0 = a + c * chunk, len = std::min(chunk, b - c0);
       pool.copy(out + c0, p->stage[k], len * sizeof(uint16_t));
       return cudaSuccess;
     };
@@ -393,22 +350,13 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
       e = ensure_stage(p, k);
       if (e == cudaSuccess) e = ensure_dbuf(p, k);
       if (e != cudaSuccess) return cuda_fail(e, "staging buffers");
-      const size_t c0 = c * chunk, len = std::min(chunk, n - c0);
-      // Halo units come from the caller's input. In place, chunks up to
-      // c - kStage have been written back by now, never c-1 or c+1 (kStage
-      // >= 2); a rewritten neighbour would be benign anyway.
-      const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
-      const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
+      const size_t c0 = a + c * chunk, len = std::min(chunk, b - c0);
       pool.copy(p->stage[k], in + c0, len * sizeof(uint16_t));
       e = cudaMemcpyAsync(p->dbuf[k], p->stage[k], len * 2, cudaMemcpyHostToDevice, p->h2d);
       if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
       cudaEventRecord(p->loaded[k], p->h2d);
       cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-      if (byte_order < 0)
-        e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, p->comp);
-      else
-        e = u16m::launch_fix_bytes(p->dbuf[k], len, p->dbuf[k], be, replacements ? p->counter : nullptr, p->comp,
-                                   left, right);
+      e = repair(p->dbuf[k], c0, len);
       if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
       cudaEventRecord(p->repaired[k], p->comp);
       cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
@@ -421,30 +369,18 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
       if (e != cudaSuccess) return cuda_fail(e, "staged D2H");
     }
     e = cudaStreamSynchronize(p->comp);
-    if (e == cudaSuccess && replacements)
-      e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "host pipeline sync");
     return U16M_OK;
   }
-  // Write-back mode (A/B): the host buffer already holds the input, so
-  // instead of a D2H copy of every chunk the kernel stores only the 32-byte
-  // groups that hold a rewrite straight into host memory.
-  e = ensure_dbuf(p, 0);
-  if (e != cudaSuccess) return cuda_fail(e, "device chunk buffer");
-  const bool writeback = in == out && dout != nullptr && host_mode() == kHostWriteback &&
-                         ((reinterpret_cast<uintptr_t>(dout) ^ reinterpret_cast<uintptr_t>(p->dbuf[0])) & 15u) == 0;
+  // Pinned: every chunk is DMA'd straight between the caller's buffer and a
+  // device ring slot; chunk c's H2D waits only for the D2H that last used its
+  // slot, so both copy engines stay busy while the kernel runs between them.
   size_t c = 0;
-  const size_t chunk = pipe_chunk_units();
-  for (size_t c0 = 0; c0 < n; c0 += chunk, c++) {
-    const size_t len = std::min(chunk, n - c0);
+  for (size_t c0 = a; c0 < b; c0 += chunk, c++) {
+    const size_t len = std::min(chunk, b - c0);
     const int k = static_cast<int>(c % kRing);
-    // Halo units are read from the host copy at enqueue time. For in-place
-    // jobs an earlier chunk's write-back may already have rewritten in[c0-1];
-    // that is benign (a unit is only rewritten when no neighbour pairs with it).
-    const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
-    const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
     if (c >= static_cast<size_t>(kRing)) {
-      e = cudaStreamWaitEvent(p->h2d, writeback ? p->repaired[k] : p->drained[k], 0);
+      e = cudaStreamWaitEvent(p->h2d, p->drained[k], 0);
       if (e != cudaSuccess) return cuda_fail(e, "pipeline wait");
     }
     e = ensure_dbuf(p, k);
@@ -453,17 +389,9 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
     cudaEventRecord(p->loaded[k], p->h2d);
     cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-    if (writeback)
-      e = u16m::launch_stream_writeback(p->dbuf[k], len, dout + c0, left, right, be,
-                                        replacements ? p->counter : nullptr, p->comp);
-    else if (byte_order < 0)
-      e = u16m::launch_repair(p->dbuf[k], len, p->dbuf[k], left, right, nullptr, nullptr, p->comp);
-    else
-      e = u16m::launch_fix_bytes(p->dbuf[k], len, p->dbuf[k], be, replacements ? p->counter : nullptr, p->comp,
-                                 left, right);
+    e = repair(p->dbuf[k], c0, len);
     if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
     cudaEventRecord(p->repaired[k], p->comp);
-    if (writeback) continue;
     cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
     e = cudaMemcpyAsync(out + c0, p->dbuf[k], len * 2, cudaMemcpyDeviceToHost, p->d2h);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
@@ -472,14 +400,119 @@ static u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, in
   e = cudaStreamSynchronize(p->d2h);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->h2d);
-  if (e == cudaSuccess && replacements)
-    e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "host pipeline sync");
   return U16M_OK;
 }
 
+// One device's whole share of a host job: select the device on this thread,
+// take its pipeline, reset its counter, run the range, read the count back.
+u16m_status host_device_job(int dev, const uint16_t* in, size_t n, uint16_t* out, size_t a, size_t b,
+                            int byte_order, unsigned long long* replacements) {
+  cudaError_t e = cudaSetDevice(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  u16m_status st = U16M_OK;
+  HostPipe* p = pipe_for(dev, &st);
+  if (p == nullptr) return st;
+  std::lock_guard<std::mutex> lock(p->mu);  // one staged job per device at a time
+  if (replacements) {
+    e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
+    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+  }
+  st = host_range(p, in, n, out, a, b, byte_order, replacements != nullptr);
+  if (st == U16M_OK && replacements) {
+    e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "replacement count");
+  }
+  return st;
+}
+
+// Smallest share worth a device of its own (a 64 MiB share is ~1.4 ms of
+// PCIe time; below that a thread + device switch costs more than it saves).
+constexpr size_t kMinUnitsPerDevice = size_t(32) << 20;
+
+// Shared body of the host-memory entry points. byte_order < 0: plain repair
+// (units in host order); 0/1: codec-fused repair in LE/BE byte order with an
+// optional replacement count (host pointer). `devs`: the devices to spread
+// the job over in contiguous ranges (one host thread per extra device), or
+// nullptr = the calling thread's current device.
+u16m_status host_pipeline(const uint16_t* in, size_t n, uint16_t* out, int byte_order,
+                          unsigned long long* replacements, const std::vector<int>* devs = nullptr) {
+  U16M_TRY(check_pair(in, n, out));
+  if (replacements) *replacements = 0;
+  if (n == 0) return U16M_OK;
+  U16M_TRY(check_device_present());
+  int cur = 0;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::vector<int> use = devs ? *devs : std::vector<int>{cur};
+  const size_t g = std::max<size_t>(1, std::min(use.size(), n / kMinUnitsPerDevice));
+  use.resize(g);
+  if (g == 1) {
+    u16m_status st = host_device_job(use[0], in, n, out, 0, n, byte_order, replacements);
+    cudaSetDevice(cur);
+    return st;
+  }
+  // Contiguous ranges, 4096-unit aligned: each device streams its own range
+  // over its own PCIe link. Ranges meet only through the halo units, read
+  // from the caller's input (benign in place, see host_range).
+  std::vector<size_t> bounds(g + 1);
+  for (size_t k = 0; k <= g; k++) bounds[k] = k == g ? n : (n / g * k) & ~size_t(4095);
+  std::vector<u16m_status> sts(g, U16M_OK);
+  std::vector<unsigned long long> counts(g, 0);
+  std::vector<std::string> errs(g);
+  std::vector<std::thread> pool;
+  for (size_t k = 1; k < g; k++)
+    pool.emplace_back([&, k] {
+      sts[k] = host_device_job(use[k], in, n, out, bounds[k], bounds[k + 1], byte_order,
+                               replacements ? &counts[k] : nullptr);
+      if (sts[k] != U16M_OK) errs[k] = u16m_last_error();
+    });
+  sts[0] = host_device_job(use[0], in, n, out, bounds[0], bounds[1], byte_order, replacements ? &counts[0] : nullptr);
+  if (sts[0] != U16M_OK) errs[0] = u16m_last_error();
+  for (auto& t : pool) t.join();
+  cudaSetDevice(cur);
+  for (size_t k = 0; k < g; k++)
+    if (sts[k] != U16M_OK) return fail(sts[k], "device " + std::to_string(use[k]) + ": " + errs[k]);
+  if (replacements)
+    for (unsigned long long c : counts) *replacements += c;
+  return U16M_OK;
+}
+
+u16m_status device_list(int num_devices, const int* device_ids, std::vector<int>* out) {
+  int visible = 0;
+  if (cudaGetDeviceCount(&visible) != cudaSuccess || visible == 0) {
+    cudaGetLastError();
+    return fail(U16M_ERR_NO_DEVICE, "no CUDA device visible (u16m has no CPU fallback)");
+  }
+  if (num_devices < 0) return fail(U16M_ERR_INVALID_ARGUMENT, "num_devices < 0");
+  if (num_devices == 0) {
+    for (int d = 0; d < visible; d++) out->push_back(d);
+    return U16M_OK;
+  }
+  if (device_ids == nullptr) return fail(U16M_ERR_INVALID_ARGUMENT, "device_ids is null with num_devices > 0");
+  for (int k = 0; k < num_devices; k++) {
+    if (device_ids[k] < 0 || device_ids[k] >= visible)
+      return fail(U16M_ERR_INVALID_ARGUMENT, "device id " + std::to_string(device_ids[k]) + " is not visible");
+    out->push_back(device_ids[k]);
+  }
+  return U16M_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 u16m_status u16m_to_well_formed_host(const uint16_t* in, size_t n, uint16_t* out) {
   return host_pipeline(in, n, out, -1, nullptr);
+}
+
+u16m_status u16m_to_well_formed_host_multi(const uint16_t* in, size_t n, uint16_t* out, int num_devices,
+                                           const int* device_ids) {
+  U16M_TRY(check_pair(in, n, out));
+  if (n == 0) return U16M_OK;
+  std::vector<int> devs;
+  U16M_TRY(device_list(num_devices, device_ids, &devs));
+  return host_pipeline(in, n, out, -1, nullptr, &devs);
 }
 
 u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out, int byte_order,
@@ -505,10 +538,10 @@ u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units,
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  std::lock_guard<std::mutex> lock(g_pipe_mu);
   u16m_status st = U16M_OK;
   HostPipe* p = pipe_for(dev, &st);
   if (p == nullptr) return st;
+  std::lock_guard<std::mutex> lock(p->mu);
   u16m::keep_pool_memory();
   const size_t data_bytes = n_units * sizeof(uint16_t), off_bytes = (num_strings + 1) * sizeof(int64_t);
   const size_t off_at = (data_bytes + 15) / 16 * 16;
@@ -545,10 +578,10 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  std::lock_guard<std::mutex> lock(g_pipe_mu);
   u16m_status st = U16M_OK;
   HostPipe* p = pipe_for(dev, &st);
   if (p == nullptr) return st;
+  std::lock_guard<std::mutex> lock(p->mu);
   // Chunked, read-only scan: chunk c+1 moves H2D (straight from pinned memory,
   // or through a pinned bounce buffer filled by the CopyPool) while chunk c
   // is scanned with its neighbours' units as halos; the scan stops at the

@@ -43,11 +43,6 @@ cudaError_t launch_stream_shift(Span s, uint16_t* out, int part, cudaStream_t st
 // Codec-fused form (u16m_stream.cu): same-phase buffers in little- or
 // big-endian byte order, optional device replacement counter (accumulated).
 cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long long* count, cudaStream_t stream);
-// Repair device units `in` and write back ONLY the 32-byte groups holding a
-// rewrite into `out`, which already holds the same input (the mapped host
-// buffer of an in-place host job). Same 16-byte phase required.
-cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
-                                   bool big_endian, unsigned long long* count, cudaStream_t stream);
 // Keep the device default mempool's freed blocks cached (stream-ordered
 // per-call workspaces stay cheap).
 void keep_pool_memory();

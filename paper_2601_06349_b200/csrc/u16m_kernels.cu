@@ -128,8 +128,12 @@ __global__ void __launch_bounds__(kThreads) repair_kernel(Span s, BatchArgs b, S
 
   if constexpr (kBatched) {
     // Range of the batch, read on the device (no host sync in the API).
-    const int64_t A = __ldg(b.offsets);
-    const int64_t B = __ldg(b.offsets + b.count - 1);
+    // Negative or decreasing ends are a contract error: clamp to an empty or
+    // non-negative range so they never address units before the buffer (the
+    // length-less form cannot check the far end; the caller guarantees it).
+    int64_t A = __ldg(b.offsets), B = __ldg(b.offsets + b.count - 1);
+    A = A < 0 ? 0 : A;
+    B = B < A ? A : B;
     s.lo = static_cast<uint64_t>(A) + b.phase;
     s.hi = static_cast<uint64_t>(B) + b.phase;
     s.out_units = reinterpret_cast<uint16_t*>(s.out) + s.lo;

@@ -336,20 +336,32 @@ __global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int6
 constexpr int kFirstPerThread = 4;
 constexpr uint64_t kNoStart = ~0ull;
 
+// The strings' extent [A, B) clamped to the caller's buffer [0, n_units):
+// offsets outside it are a contract error and must never turn into
+// out-of-bounds accesses (negative, past the end, or B < A -> empty).
+__device__ __forceinline__ void clamped_extent(const int64_t* offsets, uint64_t count, int64_t n_units, int64_t& A,
+                                               int64_t& B) {
+  A = __ldg(offsets);
+  B = __ldg(offsets + count - 1);
+  B = B < 0 ? 0 : (B < n_units ? B : n_units);
+  A = A < 0 ? 0 : (A < B ? A : B);
+}
+
 __global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t count, uint32_t phase,
-                                  uint64_t* __restrict__ tile_first, uint64_t nwt) {
+                                  uint64_t* __restrict__ tile_first, uint64_t nwt, int64_t n_units) {
   // Programmatic dependent launch: let the repair grid start now; its CTAs
   // issue their data loads and wait (griddepcontrol.wait) only before they
   // read this table.
   asm volatile("griddepcontrol.launch_dependents;");
   const uint64_t s0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * kFirstPerThread;
   if (s0 >= count) return;
-  const int64_t A = __ldg(offsets);
+  int64_t A, B;
+  clamped_extent(offsets, count, n_units, A, B);
   const int64_t base = ((A + phase) / 8) * 8 - phase;  // key of warp tile 0
   constexpr int64_t kTileUnits = kSWarpVecs * 8;        // one warp tile
   // Offsets outside the buffer are a contract error: clamp, never write out of bounds.
   auto tile_of = [&](int64_t p) -> uint64_t {
-    const uint64_t t = static_cast<uint64_t>(p - base) / kTileUnits;
+    const uint64_t t = p < base ? 0 : static_cast<uint64_t>(p - base) / kTileUnits;
     return t < nwt ? t : nwt - 1;
   };
   int64_t p[kFirstPerThread + 1];
@@ -395,11 +407,8 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   static_assert(kShift == 0 || !kInPlace, "in place is always the same phase");
   const int lane = threadIdx.x & 31;
   {
-    // Clamp to the caller's buffer: offsets beyond it are a contract error,
-    // and must not turn into out-of-bounds accesses.
-    int64_t A = __ldg(offsets), B = __ldg(offsets + count - 1);
-    B = B < n_units ? B : n_units;
-    A = A < B ? A : B;
+    int64_t A, B;
+    clamped_extent(offsets, count, n_units, A, B);
     s.lo = static_cast<uint64_t>(A) + phase;
     s.hi = static_cast<uint64_t>(B) + phase;
     s.out_units = kShift ? s.out_units + A : reinterpret_cast<uint16_t*>(s.out) + s.lo;
@@ -596,8 +605,8 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   e = cudaMemsetAsync(table, 0xFF, nwtiles_max * sizeof(uint64_t), stream);  // kNoStart
   if (e != cudaSuccess) return e;
   const uint64_t pthreads = (count + kFirstPerThread - 1) / kFirstPerThread;
-  tile_first_kernel<<<static_cast<unsigned>((pthreads + 255) / 256), 256, 0, stream>>>(offsets, count, ph, table,
-                                                                                       nwtiles_max);
+  tile_first_kernel<<<static_cast<unsigned>((pthreads + 255) / 256), 256, 0, stream>>>(
+      offsets, count, ph, table, nwtiles_max, static_cast<int64_t>(n_units));
   note_launch();
   const unsigned g = static_cast<unsigned>(ntiles_max);
   const int64_t nn = static_cast<int64_t>(n_units);
@@ -744,35 +753,6 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
   }
   stream_kernel<false, 1, 8, 4, false, true, true>
       <<<static_cast<unsigned>(ntiles), kSThreads, 0, stream>>>(s, count, half_tile_counts);
-  note_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_stream_writeback(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
-                                   bool big_endian, unsigned long long* count, cudaStream_t stream) {
-  if (n == 0) return cudaSuccess;
-  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
-  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
-  if ((ia ^ oa) & 15u) return cudaErrorInvalidValue;
-  const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
-  Span s;
-  s.in = reinterpret_cast<const uint4*>(ia - 2 * ph);
-  s.out = reinterpret_cast<uint4*>(oa - 2 * ph);
-  s.out_units = out;
-  s.lo = ph;
-  s.hi = ph + n;
-  s.left = left;
-  s.right = right;
-  s.left_ptr = s.right_ptr = nullptr;
-  s.tile_sel = kTilesAll;
-  s.prefetch_tiles = 0;
-  constexpr int kCtaVecs = (kSThreads / 32) * 32 * 8;
-  const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kCtaVecs - 1) / kCtaVecs;
-  const unsigned g = static_cast<unsigned>(ntiles);
-  // The in-place instantiation writes only 32-byte groups holding a rewrite,
-  // here into a different buffer that already holds the input.
-  if (big_endian) launch_codec_t<true, true>(s, g, count, stream);
-  else launch_codec_t<true, false>(s, g, count, stream);
   note_launch();
   return cudaGetLastError();
 }

@@ -101,8 +101,12 @@ __device__ __forceinline__ uint32_t lds16(uint32_t addr) {
 // Range of the job (device-side for the batched form).
 __device__ __forceinline__ void job_range(Span& s, const BatchArgsT& b, bool batched) {
   if (batched) {
-    const int64_t A = __ldg(b.offsets);
-    const int64_t B = __ldg(b.offsets + b.count - 1);
+    // Negative or decreasing ends are a contract error: clamp to an empty or
+    // non-negative range so they never address units before the buffer (the
+    // length-less form cannot check the far end; the caller guarantees it).
+    int64_t A = __ldg(b.offsets), B = __ldg(b.offsets + b.count - 1);
+    A = A < 0 ? 0 : A;
+    B = B < A ? A : B;
     s.lo = static_cast<uint64_t>(A) + b.phase;
     s.hi = static_cast<uint64_t>(B) + b.phase;
     s.out_units = reinterpret_cast<uint16_t*>(s.out) + s.lo;

@@ -3,12 +3,17 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <optional>
 #include <stdexcept>
 #include <string>
 
 #include "../../include/u16m.h"
 #include "../../include/utf16mend/driver.hpp"
+#include "u16m_abi.h"
+#include "u16m_internal.h"
 
 namespace utf16mend {
 
@@ -40,17 +45,20 @@ void sync_default() {
   if (e != cudaSuccess) throw std::runtime_error(std::string("utf16mend: ") + cudaGetErrorString(e));
 }
 
-// RAII device scratch for host-span helpers that are not on the hot path.
+// RAII device scratch for the small outputs of the device-span helpers:
+// stream-ordered on the legacy default stream from the device's pool, whose
+// freed blocks stay cached (no cudaMalloc/cudaFree per call).
 struct DeviceBuf {
   void* p = nullptr;
   explicit DeviceBuf(size_t bytes) {
-    if (bytes && cudaMalloc(&p, bytes) != cudaSuccess) {
+    u16m::keep_pool_memory();
+    if (bytes && cudaMallocAsync(&p, bytes, nullptr) != cudaSuccess) {
       cudaGetLastError();
       throw std::runtime_error("utf16mend: device allocation failed");
     }
   }
   ~DeviceBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, nullptr);
   }
   template <class T>
   T* as() const {
@@ -64,12 +72,12 @@ void copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("utf16mend: ") + cudaGetErrorString(e));
 }
 
-void validate(const std::optional<kernel_id>& kernel) {
-  if (kernel && !kernel_supported(*kernel, detect_cpu_features()))
-    throw std::invalid_argument("generic kernel lane count must be 4, 8, 16, or 32");
-}
-
 }  // namespace
+
+// ---- kernel selection: the reference's surface, value for value ------------
+// (proj/src/driver.cpp:15-108). The ids select nothing here — every id runs
+// the one sm_100a path — but they are listed, validated and chosen exactly as
+// the reference does so code that inspects them behaves the same.
 
 std::string to_string(const kernel_id& id) {
   switch (id.kind) {
@@ -77,52 +85,102 @@ std::string to_string(const kernel_id& id) {
     case kernel_kind::generic: return "generic" + std::to_string(id.lanes);
     case kernel_kind::bitmask: return id.emulated ? "bitmask-emulated" : "bitmask";
     case kernel_kind::bytesplit: return id.emulated ? "bytesplit-emulated" : "bytesplit";
-    case kernel_kind::cuda: return "cuda-sm100a";
   }
   return "?";
 }
 
 std::optional<kernel_id> parse_kernel_id(std::string_view name) {
-  if (name == "cuda-sm100a" || name == "cuda") return kernel_id::cuda();
-  if (name == "scalar") return kernel_id::scalar();
-  if (name == "generic") return kernel_id::generic();
-  if (name == "generic4") return kernel_id::generic(4);
-  if (name == "generic8") return kernel_id::generic(8);
-  if (name == "generic16") return kernel_id::generic(16);
-  if (name == "generic32") return kernel_id::generic(32);
-  if (name == "bitmask") return kernel_id::bitmask();
-  if (name == "bitmask-emulated") return kernel_id::bitmask(true);
-  if (name == "bytesplit") return kernel_id::bytesplit();
-  if (name == "bytesplit-emulated") return kernel_id::bytesplit(true);
+  static constexpr struct {
+    std::string_view name;
+    kernel_kind kind;
+    unsigned lanes;
+    bool emulated;
+  } kNames[] = {
+      {"scalar", kernel_kind::scalar, 0, false},        {"generic", kernel_kind::generic, 8, false},
+      {"generic4", kernel_kind::generic, 4, false},     {"generic8", kernel_kind::generic, 8, false},
+      {"generic16", kernel_kind::generic, 16, false},   {"generic32", kernel_kind::generic, 32, false},
+      {"bitmask", kernel_kind::bitmask, 0, false},      {"bitmask-emulated", kernel_kind::bitmask, 0, true},
+      {"bytesplit", kernel_kind::bytesplit, 0, false},  {"bytesplit-emulated", kernel_kind::bytesplit, 0, true},
+  };
+  for (const auto& e : kNames)
+    if (e.name == name) return kernel_id{e.kind, e.lanes, e.emulated};
   return std::nullopt;
 }
 
-cpu_features detect_cpu_features() { return {}; }
-
-bool kernel_supported(const kernel_id& id, const cpu_features&) {
-  // Any reference kernel name is accepted (and served by the one GPU path).
-  return id.kind != kernel_kind::generic ||
-         (id.lanes == 4 || id.lanes == 8 || id.lanes == 16 || id.lanes == 32);
+cpu_features detect_cpu_features() {
+  cpu_features f;
+#if defined(__x86_64__) || defined(__i386__)
+  f.wide_mask_registers = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
+#elif defined(__aarch64__)
+  f.byte_deinterleave = true;
+#endif
+  return f;
 }
 
-std::vector<kernel_id> available_kernels(const cpu_features&) { return {kernel_id::cuda()}; }
-std::vector<kernel_id> available_kernels() { return {kernel_id::cuda()}; }
+bool kernel_supported(const kernel_id& id, const cpu_features& features) {
+  switch (id.kind) {
+    case kernel_kind::scalar: return true;
+    case kernel_kind::generic: return id.lanes == 4 || id.lanes == 8 || id.lanes == 16 || id.lanes == 32;
+    case kernel_kind::bitmask: return id.emulated || features.wide_mask_registers;
+    case kernel_kind::bytesplit: return id.emulated || features.byte_deinterleave;
+  }
+  return false;
+}
 
-kernel_id select_kernel(const std::optional<kernel_id>& override_id, const cpu_features& f) {
-  if (override_id && !kernel_supported(*override_id, f))
-    throw std::invalid_argument("generic kernel lane count must be 4, 8, 16, or 32");
-  return kernel_id::cuda();
+std::vector<kernel_id> available_kernels(const cpu_features& features) {
+  std::vector<kernel_id> ids{kernel_id::scalar()};
+  for (unsigned lanes : {4u, 8u, 16u, 32u}) ids.push_back(kernel_id::generic(lanes));
+  if (features.wide_mask_registers) ids.push_back(kernel_id::bitmask());
+  ids.push_back(kernel_id::bitmask(true));
+  if (features.byte_deinterleave) ids.push_back(kernel_id::bytesplit());
+  ids.push_back(kernel_id::bytesplit(true));
+  return ids;
+}
+
+std::vector<kernel_id> available_kernels() { return available_kernels(detect_cpu_features()); }
+
+kernel_id select_kernel(const std::optional<kernel_id>& override_id, const cpu_features& features) {
+  if (override_id) {
+    if (kernel_supported(*override_id, features)) return *override_id;
+    switch (override_id->kind) {
+      case kernel_kind::bitmask:
+        throw std::invalid_argument(
+            "kernel 'bitmask' requires 512-bit vectors with mask registers (AVX-512F/BW), which this host does "
+            "not report");
+      case kernel_kind::bytesplit:
+        throw std::invalid_argument(
+            "kernel 'bytesplit' requires NEON deinterleaving loads, which this host does not report");
+      default:
+        throw std::invalid_argument("generic kernel lane count must be 4, 8, 16, or 32");
+    }
+  }
+  if (features.wide_mask_registers) return kernel_id::bitmask();
+  if (features.byte_deinterleave) return kernel_id::bytesplit();
+  return kernel_id::generic(8);
 }
 
 kernel_id select_kernel(const std::optional<kernel_id>& override_id) {
-  return select_kernel(override_id, detect_cpu_features());
+  static const cpu_features host = detect_cpu_features();
+  if (override_id) return select_kernel(override_id, host);
+  static const kernel_id chosen = [] {
+    if (const char* env = std::getenv("UTF16MEND_KERNEL")) {
+      const auto id = parse_kernel_id(env);
+      if (id && kernel_supported(*id, host)) return *id;
+      std::fprintf(stderr, "utf16mend: ignoring UTF16MEND_KERNEL=%s (%s); using default\n", env,
+                   id ? "unsupported on this host" : "unknown kernel name");
+    }
+    return select_kernel(std::nullopt, host);
+  }();
+  return chosen;
 }
+
+std::string backend_name() { return "cuda-sm100a"; }
 
 void to_well_formed(std::span<const char16_t> in, std::span<char16_t> out,
                     const std::optional<kernel_id>& kernel) {
   if (in.size() != out.size())
     throw std::invalid_argument("to_well_formed: input and output lengths differ");
-  validate(kernel);
+  (void)select_kernel(kernel);  // the reference's validation (and UTF16MEND_KERNEL warning)
   const auto* i = reinterpret_cast<const uint16_t*>(in.data());
   auto* o = reinterpret_cast<uint16_t*>(out.data());
   if (in.empty()) return;
@@ -131,7 +189,9 @@ void to_well_formed(std::span<const char16_t> in, std::span<char16_t> out,
     check(u16m_to_well_formed(i, in.size(), o, nullptr));
     sync_default();
   } else if (!di && !dout) {
-    check(u16m_to_well_formed_host(i, in.size(), o));
+    // every visible GPU, each over its own PCIe link (one device for jobs
+    // under 64 Mi units)
+    check(u16m_to_well_formed_host_multi(i, in.size(), o, 0, nullptr));
   } else {
     throw std::invalid_argument("to_well_formed: in and out must both be host or both be device memory");
   }
@@ -149,12 +209,45 @@ void to_well_formed_batched(std::span<const char16_t> in, std::span<const std::i
   const size_t S = offsets.size() - 1;
   const auto* i = reinterpret_cast<const uint16_t*>(in.data());
   auto* o = reinterpret_cast<uint16_t*>(out.data());
-  if (is_device(i)) {
-    check(u16m_to_well_formed_batched_n(i, in.size(), offsets.data(), S, o, nullptr));
-    sync_default();
+  const bool di = is_device(i), dout = is_device(o), doff = is_device(offsets.data());
+  if (in.empty() && !di && !doff) {
+    check(u16m_to_well_formed_batched_host(i, 0, offsets.data(), S, o));  // validates offsets
     return;
   }
-  check(u16m_to_well_formed_batched_host(i, in.size(), offsets.data(), S, o));
+  if (di != dout) throw std::invalid_argument("to_well_formed_batched: in and out must both be host or both be device memory");
+  if (!di) {
+    if (doff) throw std::invalid_argument("to_well_formed_batched: offsets are device memory but the strings are host memory");
+    check(u16m_to_well_formed_batched_host(i, in.size(), offsets.data(), S, o));
+    return;
+  }
+  // Device strings. Host offsets are validated and moved to the device; the
+  // units outside [offsets[0], offsets[S]) are copied, as the host form does.
+  std::int64_t ends[2] = {0, 0};
+  const std::int64_t* d_off = offsets.data();
+  std::optional<DeviceBuf> staged;
+  if (!doff) {
+    for (size_t s = 0; s < S; s++)
+      if (offsets[s] < 0 || offsets[s + 1] < offsets[s] || static_cast<size_t>(offsets[s + 1]) > in.size())
+        throw std::invalid_argument("to_well_formed_batched: offsets must be non-decreasing within the buffer");
+    if (offsets[0] < 0 || static_cast<size_t>(offsets[0]) > in.size())
+      throw std::invalid_argument("to_well_formed_batched: offsets must be non-decreasing within the buffer");
+    staged.emplace(offsets.size_bytes());
+    copy(staged->p, offsets.data(), offsets.size_bytes(), cudaMemcpyHostToDevice);
+    d_off = staged->as<std::int64_t>();
+    ends[0] = offsets.front();
+    ends[1] = offsets.back();
+  } else {
+    copy(&ends[0], offsets.data(), sizeof(std::int64_t), cudaMemcpyDeviceToHost);
+    copy(&ends[1], offsets.data() + S, sizeof(std::int64_t), cudaMemcpyDeviceToHost);
+    if (ends[0] < 0 || ends[1] < ends[0] || static_cast<size_t>(ends[1]) > in.size())
+      throw std::invalid_argument("to_well_formed_batched: offsets must be non-decreasing within the buffer");
+  }
+  check(u16m_to_well_formed_batched_n(i, in.size(), d_off, S, o, nullptr));
+  if (o != i) {
+    copy(o, i, static_cast<size_t>(ends[0]) * 2, cudaMemcpyDeviceToDevice);
+    copy(o + ends[1], i + ends[1], (in.size() - static_cast<size_t>(ends[1])) * 2, cudaMemcpyDeviceToDevice);
+  }
+  sync_default();
 }
 
 void fix_scalar(std::span<const char16_t> in, std::span<char16_t> out) { to_well_formed(in, out); }
@@ -206,6 +299,42 @@ std::vector<std::size_t> unpaired_surrogate_offsets(std::span<const char16_t> in
 }
 
 }  // namespace utf16mend
+
+// ---- kernel names for the C ABI / Python mirror -----------------------------
+namespace {
+int copy_out(const std::string& s, char* buf, size_t cap) {
+  if (buf && cap) {
+    const size_t k = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(buf, s.data(), k);
+    buf[k] = '\0';
+  }
+  return static_cast<int>(s.size());
+}
+}  // namespace
+
+extern "C" int u16m_kernel_names(char* buf, size_t cap) {
+  std::string s;
+  for (const auto& id : utf16mend::available_kernels()) s += (s.empty() ? "" : ",") + utf16mend::to_string(id);
+  return copy_out(s, buf, cap);
+}
+
+extern "C" int u16m_default_kernel_name(char* buf, size_t cap) {
+  return copy_out(utf16mend::to_string(utf16mend::select_kernel()), buf, cap);
+}
+
+extern "C" u16m_status u16m_select_kernel(const char* name, char* buf, size_t cap) {
+  std::optional<utf16mend::kernel_id> id;
+  if (name) {
+    id = utf16mend::parse_kernel_id(name);
+    if (!id) return u16m::abi::fail(U16M_ERR_INVALID_ARGUMENT, std::string("unknown kernel '") + name + "'");
+  }
+  try {
+    copy_out(utf16mend::to_string(utf16mend::select_kernel(id)), buf, cap);
+  } catch (const std::invalid_argument& e) {
+    return u16m::abi::fail(U16M_ERR_INVALID_ARGUMENT, e.what());
+  }
+  return U16M_OK;
+}
 
 // ---- generate_utf16le (reference datagen contract) --------------------------
 #include <random>

@@ -65,10 +65,29 @@ def halos_from_edges(edges: torch.Tensor, rank: int) -> tuple[int, int]:
     return left, right
 
 
+def select_halos(edges: torch.Tensor, rank: int) -> torch.Tensor:
+    """int32 [left, right] on the edges' device, with no host sync: the last
+    unit of the nearest NON-EMPTY shard before `rank` and the first unit of
+    the nearest non-empty shard after it, EMPTY (-1) where there is none. The
+    low 16 bits of EMPTY read as 0xFFFF, a non-surrogate, which the stencil
+    treats exactly like "outside the buffer" — so the kernel can read both
+    halos through pointers into this tensor unconditionally."""
+    world = edges.shape[0]
+    idx = torch.arange(world, device=edges.device)
+    firsts, lasts = edges[:, 0], edges[:, 1]
+    li = torch.where((idx < rank) & (lasts != EMPTY), idx, -1).max()
+    ri = torch.where((idx > rank) & (firsts != EMPTY), idx, world).min()
+    left = torch.where(li >= 0, lasts[li.clamp(min=0)], EMPTY)
+    right = torch.where(ri < world, firsts[ri.clamp(max=world - 1)], EMPTY)
+    return torch.stack([left, right]).to(torch.int32)
+
+
 def halo_pointers(edges: torch.Tensor, rank: int) -> tuple[int, int]:
     """Device addresses of the neighbours' edge units inside the gathered
     int32 edges tensor (the low 16 bits of each little-endian int32 are the
-    unit), 0 for none. Requires every shard to be non-empty."""
+    unit), 0 for none. Only valid when every shard is non-empty (an empty
+    neighbour's EMPTY entry would hide the shard beyond it; see
+    select_halos)."""
     world = edges.shape[0]
     base = edges.data_ptr()
     left = base + 4 * (2 * (rank - 1) + 1) if rank > 0 else 0
@@ -99,7 +118,7 @@ def init_process_group_for_repair(backend: str = "nccl", **kw):
 
 
 def repair_shard(shard: torch.Tensor, out: Optional[torch.Tensor] = None, group=None, compute=None,
-                 all_nonempty: bool = True, overlap: bool = True):
+                 all_nonempty: bool = False, overlap: bool = True):
     """Repair this rank's shard of the logical buffer.
 
     Default (sm_100a kernel through the C ABI, every rank's shard non-empty):
@@ -109,35 +128,42 @@ def repair_shard(shard: torch.Tensor, out: Optional[torch.Tensor] = None, group=
     then repairs the two edge tiles reading the neighbours' units straight
     from the gathered device tensor; the current stream joins the side
     stream. No host synchronisation inside the step. overlap=False runs
-    gather -> whole-shard kernel serially.
+    gather -> whole-shard kernel serially. The halos are picked on the
+    device from the gathered edges, skipping empty shards (select_halos);
+    all_nonempty=True (the caller guarantees every rank's shard is
+    non-empty) reads the neighbours' entries directly and saves those few
+    tiny kernels.
     `compute(shard, out, left, right)` replaces the kernel (CPU tests; host
     halo values)."""
     rank = dist.get_rank(group)
     out = shard if out is None else out
-    if compute is None and all_nonempty and shard.numel() > 0:
+    if compute is None:
         from . import _lib
 
+        def pointers(edges):
+            if all_nonempty:
+                return edges, halo_pointers(edges, rank)
+            sel = select_halos(edges, rank)
+            return sel, (sel.data_ptr(), sel.data_ptr() + 4)
+
+        if shard.numel() == 0:
+            gather_edges(shard, group)  # every rank joins the collective
+            return out
         main = torch.cuda.current_stream(shard.device)
         if not overlap:
-            edges = gather_edges(shard, group)
-            lp, rp = halo_pointers(edges, rank)
+            keep, (lp, rp) = pointers(gather_edges(shard, group))
             return _lib.to_well_formed_part(shard, out, _lib.PART_ALL, lp, rp)
         side = _side_stream(shard.device)
         side.wait_stream(main)
         _lib.to_well_formed_part(shard, out, _lib.PART_INTERIOR, stream=main)
         with torch.cuda.stream(side):
-            edges = gather_edges(shard, group)
-            lp, rp = halo_pointers(edges, rank)
+            keep, (lp, rp) = pointers(gather_edges(shard, group))
             _lib.to_well_formed_part(shard, out, _lib.PART_EDGES, lp, rp, stream=side)
-        edges.record_stream(side)
+        keep.record_stream(side)
         main.wait_stream(side)
         return out
     edges = gather_edges(shard, group)
     left, right = halos_from_edges(edges, rank)
-    if compute is None:
-        from . import _lib
-
-        return _lib.to_well_formed_halo(shard, out, left, right)
     return compute(shard, out, left, right)
 
 

@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "u16m.h"
+#include "utf16mend/driver.hpp"
 #include "u16m_datagen.h"
 
 namespace {
@@ -73,22 +74,6 @@ std::optional<order> parse_order(const std::string& s) {
   if (s == "be") return order::big;
   if (s == "auto") return std::nullopt;
   throw usage_error("--endianness must be le, be or auto");
-}
-
-bool known_kernel(const std::string& k) {
-  static const char* names[] = {"scalar",  "generic", "generic4", "generic8",         "generic16",
-                                "generic32", "bitmask", "bitmask-emulated", "bytesplit",
-                                "bytesplit-emulated", "cuda", "cuda-sm100a"};
-  for (const char* n : names)
-    if (k == n) return true;
-  return false;
-}
-
-void check_env_kernel() {  // proj/src/driver.cpp:97-104: unknown values warn and fall back
-  if (const char* env = std::getenv("UTF16MEND_KERNEL")) {
-    if (!known_kernel(env))
-      std::cerr << "utf16mend: ignoring UTF16MEND_KERNEL=" << env << " (unknown kernel name); using default\n";
-  }
 }
 
 void check_status(u16m_status st) {
@@ -201,6 +186,19 @@ args parse(int argc, char** argv, int first, const std::vector<std::pair<std::st
   return a;
 }
 
+// -k / UTF16MEND_KERNEL go through the library's reference-compatible
+// selection (proj/tools/main.cpp:46-50,63-77 -> proj/src/driver.cpp:71-108):
+// an unknown name is a usage error; an override the host does not support
+// throws std::invalid_argument (exit 2); without -k a bad UTF16MEND_KERNEL
+// warns and falls back. Every id runs the one GPU path.
+std::optional<utf16mend::kernel_id> kernel_option(const args& a) {
+  if (!a.has("--kernel")) return std::nullopt;
+  const std::string name = a.get("--kernel", "");
+  const auto id = utf16mend::parse_kernel_id(name);
+  if (!id) throw usage_error("unknown kernel '" + name + "'");
+  return id;
+}
+
 int cmd_fix(int argc, char** argv) {
   const args a = parse(argc, argv, 2,
                        {{"-o", "--output"}, {"-e", "--endianness"}, {"-k", "--kernel"}, {"--bom", "--bom"}},
@@ -212,8 +210,7 @@ int cmd_fix(int argc, char** argv) {
   if (!in_place && !a.has("--output")) throw usage_error("fix: one of --in-place or --output");
   const std::string bom = a.get("--bom", "preserve");
   if (bom != "preserve" && bom != "strip" && bom != "require") throw usage_error("--bom must be preserve, strip or require");
-  if (a.has("--kernel") && !known_kernel(a.get("--kernel", ""))) throw usage_error("unknown kernel '" + a.get("--kernel", "") + "'");
-  check_env_kernel();
+  (void)utf16mend::select_kernel(kernel_option(a));
   const auto explicit_order = parse_order(a.get("--endianness", "auto"));
 
   // The units are repaired where they lie in the file buffer (no decode /

@@ -58,7 +58,7 @@ def main():
     t = dev(data)
     P.to_well_formed_batched(t, torch.from_numpy(offs).cuda(), out=t)
     assert (host(t) == e).all(), "batched in place"
-    # host-memory path (staged / writeback / zerocopy per U16M_HOST_MODE), pinned buffers
+    # host-memory path (staged copy-engine pipeline), pinned buffers
     y = O.gen_config(1, 300_001, seed=8)
     pin = torch.from_numpy(y.view(np.int16).copy()).pin_memory()
     outp = torch.empty_like(pin).pin_memory()

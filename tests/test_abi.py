@@ -74,6 +74,85 @@ def test_cpp_dropin_compiles_links_runs(tmp_path):
         assert r.returncode == 3 and "no CUDA device" in r.stdout, r.stdout + r.stderr
 
 
+def _compile(tmp_path, src, name, cuda=False):
+    exe = tmp_path / name
+    cmd = ["g++", "-std=c++20", "-Wall", "-Wextra", "-Werror", "-I", INC, os.path.join(ROOT, "tests", "abi", src),
+           "-L", LIBDIR, "-lu16m", f"-Wl,-rpath,{LIBDIR}", "-o", str(exe)]
+    if cuda:
+        cmd[1:1] = ["-I", "/usr/local/cuda/include"]
+        cmd += ["-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64"]
+    subprocess.run(cmd, check=True)
+    return exe
+
+
+def test_reference_driver_tests_pass_against_dropin_header(tmp_path):
+    """proj/tests/test_driver.cpp's selection cases, ported assertion for
+    assertion (no GPU needed: selection and argument checks run before any
+    device work)."""
+    exe = _compile(tmp_path, "driver_compat.cpp", "driver_compat")
+    r = subprocess.run([str(exe), "select"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_utf16mend_kernel_env_soft_override(tmp_path):
+    """UTF16MEND_KERNEL: a supported name wins, an unknown or unsupported one
+    warns exactly as proj/src/driver.cpp:97-104 and falls back."""
+    exe = _compile(tmp_path, "driver_compat.cpp", "driver_compat")
+
+    def run(val):
+        env = dict(os.environ)
+        env.pop("UTF16MEND_KERNEL", None)
+        if val is not None:
+            env["UTF16MEND_KERNEL"] = val
+        return subprocess.run([str(exe), "env"], capture_output=True, text=True, env=env)
+
+    default = run(None)
+    assert default.returncode == 0 and default.stderr == ""
+    r = run("scalar")
+    assert r.stdout.strip() == "scalar" and r.stderr == ""
+    r = run("turbo")
+    assert r.stdout == default.stdout
+    assert r.stderr == "utf16mend: ignoring UTF16MEND_KERNEL=turbo (unknown kernel name); using default\n"
+    native = "bytesplit" if default.stdout.strip() != "bytesplit" else "bitmask"
+    r = run(native)
+    assert r.stdout == default.stdout
+    assert r.stderr == f"utf16mend: ignoring UTF16MEND_KERNEL={native} (unsupported on this host); using default\n"
+    if O.ref() is not None:
+        assert default.stdout.strip() == O.ref_default_kernel()
+
+
+@pytest.mark.gpu
+def test_reference_driver_repair_cases_on_gpu(tmp_path, golden):
+    """proj/tests/test_driver.cpp:82-113 on the GPU: every selectable kernel id
+    repairs the mixed sample in both modes, and all ids agree with scalar on
+    150 generate() inputs."""
+    _, arr = golden
+    exe = _compile(tmp_path, "driver_compat.cpp", "driver_compat")
+    hx = lambda a: ",".join(f"{int(v):x}" for v in a)  # noqa: E731
+    r = subprocess.run([str(exe), "repair", hx(arr["mixed_in"]), hx(arr["mixed_expected"])], capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_on_gpu(tmp_path, cuda):
+    """The C++ drop-in end to end on a GPU: the host-vector program
+    (cpp_dropin.cpp) exits 0, and the placement program (cpp_dropin_gpu.cpp:
+    device spans, batched with device/host offsets, host spans over more than
+    two pipeline chunks, validation on device spans) exits 0 — with the
+    default 32 Mi-unit chunks and with 64 KiB chunks."""
+    exe = _compile(tmp_path, "cpp_dropin.cpp", "cpp_dropin")
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    exe = _compile(tmp_path, "cpp_dropin_gpu.cpp", "cpp_dropin_gpu", cuda=True)
+    for chunk in (None, "64"):
+        env = dict(os.environ)
+        if chunk:
+            env["U16M_PIPE_CHUNK_KIB"] = chunk
+        r = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=600)
+        assert r.returncode == 0, (chunk, r.stdout + r.stderr)
+
+
 def test_python_errors_match_reference_bindings():
     with pytest.raises(ValueError, match="even length"):
         P.fix_utf16le(b"\x41")                          # module.cpp:25-26
@@ -82,7 +161,14 @@ def test_python_errors_match_reference_bindings():
     with pytest.raises(ValueError):
         P.generate_utf16le(4, pair_pct=1.5)             # module.cpp:83-84
     assert P.fix_utf16le(b"") == b""
-    assert P.available_kernels() == ["cuda-sm100a"]
+    native = "bytesplit" if P.default_kernel() != "bytesplit" else "bitmask"
+    with pytest.raises(ValueError, match="requires .* which this host does not report"):
+        P.fix_utf16le(b"\x41\x00", kernel=native)   # driver.cpp:73-86 via module.cpp (std::invalid_argument)
+    if O.ref() is not None:
+        # the reference's own lists on this host (module.cpp:95-106)
+        assert P.available_kernels() == O.ref_available_kernels()
+        assert P.default_kernel() == O.ref_default_kernel()
+    assert P.backend() == "cuda-sm100a"
 
 
 def test_no_cpu_fallback_without_gpu():

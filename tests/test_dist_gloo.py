@@ -87,6 +87,26 @@ def test_halos_from_edges_skips_empty():
     assert pdist.halos_from_edges(edges, 1) == (2, 3)
 
 
+def test_select_halos_matches_host_selection_with_empty_shards():
+    """The device-side halo choice (no host sync) skips empty shards exactly
+    like the host-side one; EMPTY reads as 0xFFFF, a non-surrogate, i.e.
+    'outside'. D800 | empty | DC00 must pair across the empty shard."""
+    E = pdist.EMPTY
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        world = int(rng.integers(1, 9))
+        e = [[int(a), int(b)] if rng.random() < 0.6 else [E, E]
+             for a, b in rng.integers(0, 0x10000, size=(world, 2))]
+        edges = torch.tensor(e, dtype=torch.int32)
+        for r in range(world):
+            sel = pdist.select_halos(edges, r).tolist()
+            assert tuple(sel) == pdist.halos_from_edges(edges, r)
+    edges = torch.tensor([[0x41, 0xD800], [E, E], [0xDC00, 0x41]], dtype=torch.int32)
+    assert pdist.select_halos(edges, 0).tolist() == [E, 0xDC00]
+    assert pdist.select_halos(edges, 2).tolist() == [0xD800, E]
+    assert (E & 0xFFFF) == 0xFFFF and not O.stencil([0xFFFF, 0x41]).tolist() != [0xFFFF, 0x41]
+
+
 def test_halo_pointer_offsets():
     edges = torch.zeros((4, 2), dtype=torch.int32)
     base = edges.data_ptr()

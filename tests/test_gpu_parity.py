@@ -462,6 +462,51 @@ def test_config3_full_batched(P, cuda):
 
 
 @pytest.mark.slow
+def test_config3_full_lengthless_entry(P, cuda):
+    """Full config 3 through the north-star batched signature (no buffer
+    length: u16m_to_well_formed_batched), copy and in place, against the
+    oracle's per-string fix_scalar."""
+    d, o = P._lib.gen_c3(1 << 20)
+    L = P._lib.raw()
+    s = torch.cuda.current_stream().cuda_stream
+    out = torch.empty_like(d)
+    assert L.u16m_to_well_formed_batched(d.data_ptr(), o.data_ptr(), o.numel() - 1, out.data_ptr(), s) == 0
+    e = O.fix_batched(host(d), o.cpu().numpy())
+    assert (host(out) == e).all()
+    y = d.clone()
+    assert L.u16m_to_well_formed_batched(y.data_ptr(), o.data_ptr(), o.numel() - 1, y.data_ptr(), s) == 0
+    assert torch.equal(y, out)
+
+
+def test_batched_negative_offsets_never_write_outside(P, cuda):
+    """offsets[0] < 0 is a contract error: both batched entries clamp the
+    extent to the buffer, so nothing before `in`/`out` is read or written
+    (the clamp missed A < 0)."""
+    L = P._lib.raw()
+    s = torch.cuda.current_stream().cuda_stream
+    guard = 64
+    for ph in range(8):
+        n = 50_000
+        x = O.gen_config(1, n + 2 * guard, seed=ph)
+        t = dev(x)
+        for off in (np.array([-5, 100, 4000, n], np.int64), np.array([-(1 << 40), 7, n], np.int64)):
+            o = torch.from_numpy(off).cuda()
+            out = t.clone()
+            base_in = t[guard + ph:]
+            base_out = out[guard + ph:]
+            assert L.u16m_to_well_formed_batched_n(base_in.data_ptr(), n, o.data_ptr(), o.numel() - 1,
+                                                   base_out.data_ptr(), s) == 0
+            assert L.u16m_to_well_formed_batched(base_in.data_ptr(), o.data_ptr(), o.numel() - 1,
+                                                 base_out.data_ptr(), s) == 0
+            torch.cuda.synchronize()
+            assert torch.equal(out[:guard + ph], t[:guard + ph])          # nothing before the buffer
+            clamped = off.copy()
+            clamped[0] = 0
+            seg = O.fix_batched(x[guard + ph:guard + ph + n], clamped)
+            assert (host(out[guard + ph:guard + ph + n]) == seg).all()
+
+
+@pytest.mark.slow
 def test_config4_shards(P, cuda):
     """Config 4 on one GPU: 4 virtual shards of 2^26 units with adversarial
     shard edges (exact, whole buffer) and one full 2^32-unit shard (windows)."""

@@ -20,8 +20,7 @@ VARIANTS = [
     {"U16M_KERNEL": "ldg"},
     {"U16M_KERNEL": "ldg", "U16M_GRAN": "1"},
     {"U16M_GRAN": "4", "U16M_PIPE_CHUNK_KIB": "64"},
-    {"U16M_HOST_MODE": "writeback", "U16M_PIPE_CHUNK_KIB": "64"},
-    {"U16M_HOST_MODE": "zerocopy"},
+    {"U16M_PIPE_CHUNK_KIB": "64", "U16M_HOST_THREADS": "3"},
 ]
 
 
