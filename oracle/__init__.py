@@ -84,6 +84,7 @@ def ref():
         R.ref_unpaired_surrogate_offsets.restype = _sz
         R.ref_default_kernel.argtypes = [ctypes.c_char_p, _sz]
         R.ref_available_kernels.argtypes = [ctypes.c_char_p, _sz]
+        R.ref_parse_csv.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _sz]
         _ref = R
     return _ref
 
@@ -202,3 +203,20 @@ def ref_available_kernels() -> list[str]:
     buf = ctypes.create_string_buffer(512)
     ref().ref_available_kernels(buf, 512)
     return buf.value.decode().split(",")
+
+
+def ref_parse_csv(path: str) -> list[tuple]:
+    """Parse a CSV report with the reference's own parse_csv
+    (proj/src/bench.cpp:172-203): [(impl, units, bytes, best_ns, mean_ns,
+    gbps, margin_pct)], floats exact. Raises ValueError when it throws."""
+    buf = ctypes.create_string_buffer(1 << 20)
+    k = ref().ref_parse_csv(path.encode(), buf, 1 << 20)
+    if k == -1:
+        raise FileNotFoundError(path)
+    if k < 0:
+        raise ValueError("reference parse_csv threw")
+    rows = []
+    for line in buf.value.decode().splitlines():
+        f = line.split("|")
+        rows.append((f[0], int(f[1]), int(f[2]), int(f[3]), float(f[4]), float(f[5]), float(f[6])))
+    return rows

@@ -19,6 +19,9 @@
 #include <array>
 #include <cstdint>
 #include <cstring>
+#include <cstdio>
+#include <fstream>
+#include <sstream>
 #include <optional>
 #include <span>
 #include <string>
@@ -26,6 +29,7 @@
 #include <vector>
 
 #include "test_helpers.hpp"
+#include "utf16mend/bench.hpp"
 #include "utf16mend/datagen.hpp"
 #include "utf16mend/driver.hpp"
 #include "utf16mend/surrogate.hpp"
@@ -171,6 +175,31 @@ size_t ref_unpaired_surrogate_offsets(const uint16_t* in, size_t n, size_t limit
       std::span<const char16_t>(reinterpret_cast<const char16_t*>(in), n), limit);
   for (size_t i = 0; i < v.size(); i++) out[i] = v[i];
   return v.size();
+}
+
+// The reference's own CSV reader (proj/src/bench.cpp:172-203) over a file:
+// one line per parsed point, "impl|input_units|bytes|best_ns|mean_ns|gbps|
+// error_margin_pct" with %.17g (exact round trip). Returns the full length,
+// -1 when the file cannot be opened, -2 when parse_csv throws.
+int ref_parse_csv(const char* path, char* buf, size_t cap) {
+  std::ifstream in(path);
+  if (!in) return -1;
+  try {
+    const auto series = parse_csv(in);
+    std::string s;
+    char line[512];
+    for (const auto& sr : series)
+      for (const auto& p : sr.points) {
+        const auto& r = p.result;
+        std::snprintf(line, sizeof line, "%s|%zu|%zu|%llu|%.17g|%.17g|%.17g\n", r.impl_name.c_str(), r.input_units,
+                      r.bytes_per_rep, static_cast<unsigned long long>(r.best_ns), r.mean_ns, r.throughput_gbps,
+                      r.error_margin_pct);
+        s += line;
+      }
+    return copy_string(s, buf, cap);
+  } catch (...) {
+    return -2;
+  }
 }
 
 int ref_default_kernel(char* buf, size_t cap) { return copy_string(to_string(select_kernel()), buf, cap); }
