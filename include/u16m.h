@@ -56,8 +56,11 @@ u16m_status u16m_to_well_formed_in_place(uint16_t* buf, size_t n, void* stream);
  * [offsets[s], offsets[s+1]) for s < num_strings is repaired independently —
  * string edges are "outside", so no pairing across strings. `offsets` is a
  * DEVICE array of num_strings+1 non-decreasing int64 unit indices into
- * in/out; units outside [offsets[0], offsets[num_strings]) are untouched.
- * out may equal in. */
+ * in/out (a negative offsets[0] is clamped to 0; offsets past the end of the
+ * buffers are undefined behaviour — use the _n form to have them clamped);
+ * units outside [offsets[0], offsets[num_strings]) are untouched.
+ * out may equal in. No host synchronisation: the grid is sized from the
+ * device allocations holding in/out (cuMemGetAddressRange). */
 u16m_status u16m_to_well_formed_batched(const uint16_t* in, const int64_t* offsets,
                                         size_t num_strings, uint16_t* out, void* stream);
 

@@ -10,6 +10,7 @@
 // U16M_ERR_NO_DEVICE (the reference throws std::runtime_error when a native
 // backend is missing, proj/src/bitmask_kernel.cpp:102-104).
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -72,6 +73,34 @@ u16m_status check_pair(const uint16_t* in, size_t n, const uint16_t* out) {
 }
 
 }  // namespace u16m::abi
+
+namespace u16m {
+
+// Units from `p` to the end of the device allocation holding it (driver
+// cuMemGetAddressRange through the runtime's entry-point query, so the
+// library needs no libcuda link), 0 when unknown.
+size_t allocation_units_after(const void* p) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return Fn(nullptr);
+    }
+    return reinterpret_cast<Fn>(f);
+  }();
+  if (fn == nullptr || p == nullptr) return 0;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return 0;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if (a < base || a >= base + size) return 0;
+  return (base + size - a) / sizeof(uint16_t);
+}
+
+}  // namespace u16m
 
 using namespace u16m::abi;
 
@@ -185,7 +214,20 @@ u16m_status u16m_to_well_formed_batched(const uint16_t* in, const int64_t* offse
   U16M_TRY(check_device_ptr(in, "in"));
   if (out != in) U16M_TRY(check_device_ptr(out, "out"));
   U16M_TRY(check_device_ptr(offsets, "offsets"));
-  const cudaError_t e = u16m::launch_batched(in, offsets, num_strings, out, as_stream(stream));
+  // The caller gave no buffer length, and reading offsets[S] back would cost
+  // a host sync. The allocations holding `in` and `out` bound it instead
+  // (cuMemGetAddressRange): the register-staged tile kernel of the
+  // length-aware form runs with its grid sized from that bound (CTAs past
+  // offsets[S] exit at once). When the bound is unknown (not a cudaMalloc'd
+  // range) or loose enough that idle CTAs could cost more than the tile form
+  // saves (> 4 GiB past `in`), the persistent TMA kernel runs instead: its
+  // grid is the SM count and it reads the range on the device.
+  const size_t bound = std::min(u16m::allocation_units_after(in), u16m::allocation_units_after(out));
+  cudaError_t e;
+  if (bound > 0 && bound <= (size_t(1) << 31) && u16m::batched_tiles_enabled())
+    e = u16m::launch_batched_tiles(in, bound, offsets, num_strings, out, as_stream(stream));
+  else
+    e = u16m::launch_batched(in, offsets, num_strings, out, as_stream(stream));
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "batched repair kernel launch");
 }
 

@@ -70,6 +70,9 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
                                     unsigned long long* offsets_out, unsigned long long* count_out,
                                     cudaStream_t stream, int32_t left = -1, int32_t right = -1);
 
+// Units from p to the end of its device allocation (0 = unknown).
+size_t allocation_units_after(const void* p);
+
 unsigned long long launch_count();
 void note_launch();
 

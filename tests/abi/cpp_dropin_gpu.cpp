@@ -12,6 +12,7 @@
 // Exit 0 = all correct; 1 = wrong result; 2 = wrong/missing exception.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -101,7 +102,8 @@ int main() {
       const size_t n = 300000;
       const auto x = random_units(n, 11);
       std::vector<std::int64_t> offs{17};
-      while (offs.back() < static_cast<std::int64_t>(n) - 500) offs.push_back(offs.back() + 1 + (offs.size() * 7919) % 3000);
+      while (offs.back() < static_cast<std::int64_t>(n) - 500)
+        offs.push_back(std::min<std::int64_t>(offs.back() + 1 + (offs.size() * 7919) % 3000, n - 100));
       std::vector<char16_t> e = x;  // units outside [offs.front(), offs.back()) unchanged
       for (size_t s = 0; s + 1 < offs.size(); s++) {
         const auto part = stencil(x, offs[s], offs[s + 1]);
