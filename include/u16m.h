@@ -162,6 +162,11 @@ u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out,
                                       unsigned long long* replacements);
 u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,
                                        unsigned long long* offsets_out, size_t* count_out);
+/* Same over raw UTF-16 bytes in the given byte order (CLI `check` of a
+ * big-endian file, proj/tools/main.cpp:96-115): big-endian chunks are
+ * byte-swapped on the device after their H2D copy. */
+u16m_status u16m_unpaired_offsets_bytes_host(const void* in, size_t n_units, int byte_order, size_t limit,
+                                             unsigned long long* offsets_out, size_t* count_out);
 /* Batched form on host memory (behind the C++ to_well_formed_batched on host
  * spans): `in`/`out` hold n_units units (equal or disjoint), `offsets` (host)
  * num_strings + 1 non-decreasing entries within [0, n_units]. Synchronous. */

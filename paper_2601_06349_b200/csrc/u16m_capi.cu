@@ -132,6 +132,27 @@ bool ensure_peer(int from, int to) {
   return true;
 }
 
+// Non-blocking streams for the shard driver, created once per (device, slot)
+// and kept for the process: shards on distinct devices run concurrently, and
+// up to kShardSlots shards on one device (virtual shards) too. A call no
+// longer creates and destroys a stream per shard.
+constexpr int kShardSlots = 8;
+std::mutex g_stream_mu;
+std::vector<std::pair<int, cudaStream_t>> g_streams;  // (device * kShardSlots + slot, stream)
+
+cudaError_t cached_stream(int dev, int k, cudaStream_t* out) {
+  const int key = dev * kShardSlots + (k % kShardSlots);
+  std::lock_guard<std::mutex> lock(g_stream_mu);
+  for (auto& e : g_streams)
+    if (e.first == key) {
+      *out = e.second;
+      return cudaSuccess;
+    }
+  const cudaError_t e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);  // on the current device (dev)
+  if (e == cudaSuccess) g_streams.emplace_back(key, *out);
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -321,46 +342,46 @@ u16m_status u16m_to_well_formed_sharded(int num_shards, const int* device_ids,
   }
   // Halo pointers: the last unit of the previous non-empty shard and the first
   // unit of the next one, read by the kernel directly (same device, or a peer
-  // over NVLink). Without peer access the unit is fetched by value.
+  // over NVLink). Without peer access the two units are copied peer-to-peer,
+  // stream-ordered, into a small scratch on the shard's device first.
   std::vector<cudaStream_t> streams(num_shards, nullptr);
+  std::vector<uint16_t*> scratch(num_shards, nullptr);
   u16m_status st = U16M_OK;
   for (int g = 0; g < num_shards && st == U16M_OK; g++) {
     if (shard_len[g] == 0) continue;
     const int dev = device_ids[g];
+    int k = 0;
+    for (int h = 0; h < g; h++) k += (streams[h] != nullptr && device_ids[h] == dev);
     int lk = g - 1, rk = g + 1;
     while (lk >= 0 && shard_len[lk] == 0) lk--;
     while (rk < num_shards && shard_len[rk] == 0) rk++;
     const uint16_t* lp = lk >= 0 ? shard_in[lk] + shard_len[lk] - 1 : nullptr;
     const uint16_t* rp = rk < num_shards ? shard_in[rk] : nullptr;
-    int32_t lv = -1, rv = -1;
-    if (lp && !ensure_peer(dev, device_ids[lk])) {
-      uint16_t u = 0;
-      cudaSetDevice(device_ids[lk]);
-      cudaError_t e = cudaMemcpy(&u, lp, 2, cudaMemcpyDeviceToHost);
-      if (e != cudaSuccess) { st = cuda_fail(e, "halo fetch"); break; }
-      lv = u;
-      lp = nullptr;
-    }
-    if (rp && !ensure_peer(dev, device_ids[rk])) {
-      uint16_t u = 0;
-      cudaSetDevice(device_ids[rk]);
-      cudaError_t e = cudaMemcpy(&u, rp, 2, cudaMemcpyDeviceToHost);
-      if (e != cudaSuccess) { st = cuda_fail(e, "halo fetch"); break; }
-      rv = u;
-      rp = nullptr;
-    }
+    const bool lpeer = !lp || ensure_peer(dev, device_ids[lk]);
+    const bool rpeer = !rp || ensure_peer(dev, device_ids[rk]);
     cudaSetDevice(dev);
-    cudaError_t e = cudaStreamCreateWithFlags(&streams[g], cudaStreamNonBlocking);
-    if (e != cudaSuccess) { st = cuda_fail(e, "stream create"); break; }
-    e = u16m::launch_repair(shard_in[g], shard_len[g], shard_out[g], lv, rv, lp, rp, streams[g]);
+    cudaError_t e = cached_stream(dev, k, &streams[g]);
+    if (e != cudaSuccess) { st = cuda_fail(e, "shard stream"); break; }
+    if (!lpeer || !rpeer) {
+      u16m::keep_pool_memory();
+      e = cudaMallocAsync(reinterpret_cast<void**>(&scratch[g]), 4, streams[g]);
+      if (e == cudaSuccess && !lpeer)
+        e = cudaMemcpyPeerAsync(scratch[g], dev, lp, device_ids[lk], 2, streams[g]);
+      if (e == cudaSuccess && !rpeer)
+        e = cudaMemcpyPeerAsync(scratch[g] + 1, dev, rp, device_ids[rk], 2, streams[g]);
+      if (e != cudaSuccess) { st = cuda_fail(e, "halo fetch"); break; }
+      if (!lpeer) lp = scratch[g];
+      if (!rpeer) rp = scratch[g] + 1;
+    }
+    e = u16m::launch_repair(shard_in[g], shard_len[g], shard_out[g], -1, -1, lp, rp, streams[g]);
     if (e != cudaSuccess) { st = cuda_fail(e, "shard kernel launch"); break; }
   }
   for (int g = 0; g < num_shards; g++) {
     if (!streams[g]) continue;
     cudaSetDevice(device_ids[g]);
+    if (scratch[g]) cudaFreeAsync(scratch[g], streams[g]);
     const cudaError_t e = cudaStreamSynchronize(streams[g]);
     if (e != cudaSuccess && st == U16M_OK) st = cuda_fail(e, "shard sync");
-    cudaStreamDestroy(streams[g]);
   }
   cudaSetDevice(prev);
   return st;

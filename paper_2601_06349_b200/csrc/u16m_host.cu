@@ -565,8 +565,15 @@ u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units,
   return U16M_OK;
 }
 
-u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,
-                                       unsigned long long* offsets_out, size_t* count_out) {
+}  // extern "C"
+
+namespace {
+
+// Chunked host validation scan; byte_order < 0: units in host order, else the
+// bytes' order (big-endian chunks are byte-swapped on the device after their
+// H2D copy).
+u16m_status unpaired_offsets_host(const uint16_t* in, size_t n, int byte_order, size_t limit,
+                                  unsigned long long* offsets_out, size_t* count_out) {
   if (count_out == nullptr || (limit > 0 && offsets_out == nullptr))
     return fail(U16M_ERR_INVALID_ARGUMENT, "null output");
   *count_out = 0;
@@ -589,6 +596,11 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
   // is_well_formed for 1), so an ill-formed buffer is rarely read to its end.
   const bool pinned = is_pinned(in);
   const size_t chunk = pipe_chunk_units();
+  const bool be = byte_order == U16M_BIG_ENDIAN;
+  auto unit = [&](size_t i) -> int32_t {
+    const uint32_t w = in[i];
+    return static_cast<int32_t>(be ? (((w & 0xFFu) << 8) | (w >> 8)) : w);
+  };
 
   const size_t cap = std::min(limit, chunk);
   void* ws = nullptr;
@@ -610,6 +622,7 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
       src = p->stage[k];
     }
     r = cudaMemcpyAsync(p->dbuf[k], src, len * 2, cudaMemcpyHostToDevice, p->h2d);
+    if (r == cudaSuccess && be) r = u16m::launch_byteswap(p->dbuf[k], len, p->h2d);
     if (r == cudaSuccess) cudaEventRecord(p->loaded[k], p->h2d);
     return r;
   };
@@ -622,8 +635,8 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
     if (c + 1 < nchunks) e = load(c + 1);
     if (e != cudaSuccess) break;
     cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-    const int32_t left = c0 > 0 ? in[c0 - 1] : -1;
-    const int32_t right = c0 + len < n ? in[c0 + len] : -1;
+    const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
+    const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
     e = u16m::launch_unpaired_offsets(p->dbuf[k], len, std::min(limit - found, cap), d_off, d_cnt, p->comp,
                                       left, right);
     if (e != cudaSuccess) break;
@@ -643,6 +656,22 @@ u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limi
   if (f != cudaSuccess) return cuda_fail(f, "unpaired offsets");
   *count_out = found;
   return U16M_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,
+                                       unsigned long long* offsets_out, size_t* count_out) {
+  return unpaired_offsets_host(in, n, -1, limit, offsets_out, count_out);
+}
+
+u16m_status u16m_unpaired_offsets_bytes_host(const void* in, size_t n_units, int byte_order, size_t limit,
+                                             unsigned long long* offsets_out, size_t* count_out) {
+  if (byte_order != U16M_LITTLE_ENDIAN && byte_order != U16M_BIG_ENDIAN)
+    return fail(U16M_ERR_INVALID_ARGUMENT, "byte_order must be U16M_LITTLE_ENDIAN or U16M_BIG_ENDIAN");
+  return unpaired_offsets_host(static_cast<const uint16_t*>(in), n_units, byte_order, limit, offsets_out, count_out);
 }
 
 }  // extern "C"

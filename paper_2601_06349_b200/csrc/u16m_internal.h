@@ -70,6 +70,9 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
                                     unsigned long long* offsets_out, unsigned long long* count_out,
                                     cudaStream_t stream, int32_t left = -1, int32_t right = -1);
 
+// In-place byte swap of n units (p 16-byte aligned).
+cudaError_t launch_byteswap(uint16_t* p, size_t n, cudaStream_t stream);
+
 // Units from p to the end of its device allocation (0 = unknown).
 size_t allocation_units_after(const void* p);
 

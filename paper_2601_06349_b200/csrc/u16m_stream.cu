@@ -789,6 +789,36 @@ cudaError_t launch_stream_shift(Span s, uint16_t* out, int part, cudaStream_t st
   return cudaGetLastError();
 }
 
+// Byte swap of n units in place (p 16-byte aligned): the big-endian form of
+// the host validation scan swaps each chunk on the device after its H2D copy
+// (HBM-speed, hidden under the PCIe transfer of the next chunk) instead of on
+// one host thread.
+__global__ void byteswap_kernel(uint4* __restrict__ p, uint64_t nvec, uint16_t* __restrict__ tail, uint32_t ntail) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < nvec) {
+    uint4 v = p[i];
+    v.x = prmt(v.x, 0, 0x2301);
+    v.y = prmt(v.y, 0, 0x2301);
+    v.z = prmt(v.z, 0, 0x2301);
+    v.w = prmt(v.w, 0, 0x2301);
+    p[i] = v;
+  } else if (i - nvec < ntail) {
+    const uint32_t u = tail[i - nvec];
+    tail[i - nvec] = static_cast<uint16_t>((u >> 8) | (u << 8));
+  }
+}
+
+cudaError_t launch_byteswap(uint16_t* p, size_t n, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const uint64_t nvec = n / 8;
+  const uint32_t ntail = static_cast<uint32_t>(n % 8);
+  const uint64_t total = nvec + ntail;
+  byteswap_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(reinterpret_cast<uint4*>(p), nvec,
+                                                                                   p + nvec * 8, ntail);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream) {
   return launch_stream_v<kSV, 4>(s, part, stream);
 }

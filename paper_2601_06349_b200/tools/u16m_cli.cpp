@@ -250,19 +250,13 @@ int cmd_check(int argc, char** argv) {
   if (!explicit_order && !d.had_bom)
     std::cerr << "utf16mend: " << path << ": no BOM found, assuming little-endian\n";
   const size_t n = d.n_units;
-  // Little-endian units are scanned where they lie in the file buffer; a
-  // big-endian file is byte-swapped into host order first.
-  std::vector<uint16_t> swapped;
-  const uint16_t* units = reinterpret_cast<const uint16_t*>(bytes.data() + d.start);
-  if (d.byte_order == order::big) {
-    swapped.resize(n);
-    const uint8_t* b = bytes.data() + d.start;
-    for (size_t i = 0; i < n; i++) swapped[i] = static_cast<uint16_t>((b[2 * i] << 8) | b[2 * i + 1]);
-    units = swapped.data();
-  }
+  // The units are scanned where they lie in the file buffer, in the file's
+  // byte order (big-endian chunks are swapped on the device).
   unsigned long long offs[10];
   size_t count = 0;
-  check_status(u16m_unpaired_offsets_host(units, n, 10, offs, &count));
+  check_status(u16m_unpaired_offsets_bytes_host(bytes.data() + d.start, n,
+                                                d.byte_order == order::big ? U16M_BIG_ENDIAN : U16M_LITTLE_ENDIAN,
+                                                10, offs, &count));
   if (count == 0) {
     std::cout << path << ": well-formed\n";
     return 0;

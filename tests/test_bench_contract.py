@@ -27,18 +27,29 @@ def test_reference_arm_contract():
     assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["config"]["units_per_gpu"] == 1 << 24 and d["modes"]["copy"]["value"] == d["value"]
 
 
 @pytest.mark.gpu
 def test_gpu_arm_contract(cuda):
-    d = run_bench("--steps", "5", "--warmup", "3")
+    """The default line: config 4 (2^32 units/GPU), copy headline + in place,
+    roofline / cpu_baseline / e2e / clocks / gpu_launches present, the same
+    `config` dict the reference arm prints."""
+    d = run_bench("--steps", "5", "--warmup", "3", timeout=1200)
     assert BASE_KEYS <= set(d)
     assert d["n_gpus"] == 1 and d["higher_is_better"] is True and d["scaling"] == "weak"
+    c = d["config"]
+    assert c["config_id"] == 4 and c["units_per_gpu"] == 1 << 32 and c["modes"] == ["copy", "inplace"]
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
-    e = d["e2e"]
-    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * d["config"]["units_per_gpu"]
+    for m in ("copy", "inplace"):
+        md = d["modes"][m]
+        assert md["output_check_well_formed"] is True and md["gpu_launches"] == 5
+        e = md["e2e"]
+        assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * c["units_per_gpu"] and e["matches_device_result"]
+    assert d["e2e"] == d["modes"]["copy"]["e2e"] and d["value"] == d["modes"]["copy"]["value"]
     assert d["gpu_launches"] == 5
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
-    assert d["config"]["output_check_well_formed"] is True
+    ref = run_bench("--impl", "reference", "--steps", "2", "--warmup", "3", timeout=1200)
+    assert ref["config"] == c
