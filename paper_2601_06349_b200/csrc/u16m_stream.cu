@@ -819,7 +819,29 @@ cudaError_t launch_byteswap(uint16_t* p, size_t n, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// Small copy jobs (a few waves of 32 KiB tiles, e.g. config 0's 32 MiB =
+// 1.7 waves) lose their last partial wave; U16M_SMALL_SV (A/B, 0 = off)
+// runs them with fewer vectors per thread: more, shorter CTAs.
+static int small_sv_setting() {
+  static const int v = [] {
+    const char* e = std::getenv("U16M_SMALL_SV");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream) {
+  const int sv = small_sv_setting();
+  if (sv && s.in != s.out && part == kTilesAll) {
+    const uint64_t nvec = (s.hi + 7) / 8 - s.lo / 8;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (nvec <= static_cast<uint64_t>(4 * sms * 4) * kSCtaVecs) {
+      if (sv == 4) return launch_stream_v<4, 4>(s, part, stream);
+      if (sv == 46) return launch_stream_v<4, 6>(s, part, stream);
+      if (sv == 28) return launch_stream_v<2, 8>(s, part, stream);
+    }
+  }
   return launch_stream_v<kSV, 4>(s, part, stream);
 }
 
