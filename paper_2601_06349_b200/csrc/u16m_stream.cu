@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -347,6 +348,16 @@ __device__ __forceinline__ void clamped_extent(const int64_t* offsets, uint64_t 
   A = A < 0 ? 0 : (A < B ? A : B);
 }
 
+// The table's "no start" fill, as the primary of a programmatic dependent
+// launch chain fill -> tile_first_kernel -> batched_tile_kernel (a
+// cudaMemsetAsync cannot start its successor early).
+__global__ void table_fill_kernel(uint4* __restrict__ t, uint64_t n16) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    t[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+}
+
 __global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t count, uint32_t phase,
                                   uint64_t* __restrict__ tile_first, uint64_t nwt, int64_t n_units) {
   // Programmatic dependent launch: let the repair grid start now; its CTAs
@@ -354,7 +365,10 @@ __global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t 
   // read this table.
   asm volatile("griddepcontrol.launch_dependents;");
   const uint64_t s0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * kFirstPerThread;
-  if (s0 >= count) return;
+  if (s0 >= count) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   int64_t A, B;
   clamped_extent(offsets, count, n_units, A, B);
   const int64_t base = ((A + phase) / 8) * 8 - phase;  // key of warp tile 0
@@ -368,6 +382,8 @@ __global__ void tile_first_kernel(const int64_t* __restrict__ offsets, uint64_t 
   p[0] = s0 ? __ldg(offsets + s0 - 1) : 0;
 #pragma unroll
   for (int j = 0; j < kFirstPerThread; j++) p[j + 1] = s0 + j < count ? __ldg(offsets + s0 + j) : 0;
+  // the "no start" fill (the primary grid) is complete and visible from here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < kFirstPerThread; j++) {
     const uint64_t si = s0 + j;
@@ -597,31 +613,38 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   constexpr uint64_t kTileUnits = kSCtaVecs * 8;
   const uint64_t count = static_cast<uint64_t>(num_strings) + 1;
   const uint64_t ntiles_max = (static_cast<uint64_t>(n_units) + 16) / kTileUnits + 2;
-  const uint64_t nwtiles_max = ntiles_max * (kSThreads / 32);
+  const uint64_t nwtiles_max = ntiles_max * (kSThreads / 32);  // even
   uint64_t* table = nullptr;  // first string starting in or after each warp tile
   keep_pool_memory();
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&table), nwtiles_max * sizeof(uint64_t), stream);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(table, 0xFF, nwtiles_max * sizeof(uint64_t), stream);  // kNoStart
-  if (e != cudaSuccess) return e;
-  const uint64_t pthreads = (count + kFirstPerThread - 1) / kFirstPerThread;
-  tile_first_kernel<<<static_cast<unsigned>((pthreads + 255) / 256), 256, 0, stream>>>(
-      offsets, count, ph, table, nwtiles_max, static_cast<int64_t>(n_units));
-  note_launch();
-  const unsigned g = static_cast<unsigned>(ntiles_max);
-  const int64_t nn = static_cast<int64_t>(n_units);
-  // Launched as a programmatic dependent of tile_first_kernel (PDL): the grid
-  // is scheduled while the pre-pass still runs.
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g);
-  cfg.blockDim = dim3(kSThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = stream;
+  // kNoStart fill (nwtiles_max is even: 16-byte stores) -> pre-pass -> repair,
+  // each a programmatic dependent of the previous: a grid is scheduled while
+  // its predecessor still runs and waits only where it reads its results.
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = batched_pdl() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const uint64_t n16 = nwtiles_max / 2;
+  table_fill_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n16 + 255) / 256, 148 * 8)), 256, 0, stream>>>(
+      reinterpret_cast<uint4*>(table), n16);
+  note_launch();
+  const uint64_t pthreads = (count + kFirstPerThread - 1) / kFirstPerThread;
+  cfg.gridDim = dim3(static_cast<unsigned>((pthreads + 255) / 256));
+  e = cudaLaunchKernelEx(&cfg, tile_first_kernel, offsets, count, ph, static_cast<uint64_t*>(table), nwtiles_max,
+                         static_cast<int64_t>(n_units));
+  if (e != cudaSuccess) return e;
+  note_launch();
+  const unsigned g = static_cast<unsigned>(ntiles_max);
+  const int64_t nn = static_cast<int64_t>(n_units);
+  // The repair grid: a programmatic dependent of tile_first_kernel.
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(kSThreads);
   const uint64_t cnt = count, nwt = nwtiles_max;
   const uint64_t* tab = table;
   const int64_t q0 = 0;
@@ -819,29 +842,11 @@ cudaError_t launch_byteswap(uint16_t* p, size_t n, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-// Small copy jobs (a few waves of 32 KiB tiles, e.g. config 0's 32 MiB =
-// 1.7 waves) lose their last partial wave; U16M_SMALL_SV (A/B, 0 = off)
-// runs them with fewer vectors per thread: more, shorter CTAs.
-static int small_sv_setting() {
-  static const int v = [] {
-    const char* e = std::getenv("U16M_SMALL_SV");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
+// Small copy jobs (config 0: 32 MiB = 1.73 waves of 32 KiB tiles) keep the
+// same tiles: 16 KiB tiles (3.5 waves), 28 KiB tiles (1.98 waves), 8 CTAs/SM
+// with 8 KiB tiles and an earlier L2 prefetch all measured slower (14.5 us
+// vs 15.8-18.5 us, profiles/README.md).
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream) {
-  const int sv = small_sv_setting();
-  if (sv && s.in != s.out && part == kTilesAll) {
-    const uint64_t nvec = (s.hi + 7) / 8 - s.lo / 8;
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (nvec <= static_cast<uint64_t>(4 * sms * 4) * kSCtaVecs) {
-      if (sv == 4) return launch_stream_v<4, 4>(s, part, stream);
-      if (sv == 46) return launch_stream_v<4, 6>(s, part, stream);
-      if (sv == 28) return launch_stream_v<2, 8>(s, part, stream);
-    }
-  }
   return launch_stream_v<kSV, 4>(s, part, stream);
 }
 
