@@ -294,9 +294,12 @@ def run_reference(args):
         res[mode] = time_cpu(args.config, per_gpu, mode, reps=args.steps, warmup=args.warmup, budget_s=240.0,
                              data=data)
     head = res[modes[0]]
-    sample = (f"{head['units']} units of {args.config} per rep (full config), {head['reps']} timed reps after "
-              f"{args.warmup} warm-up; value = units x reps / summed rep time; in place restored before every rep "
-              "(outside the timing)")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    sample = (f"{head['units']} units of {args.config} per rep (full config"
+              + (f"; one shard's worth: the CPU rate does not depend on how the {world}-shard job is split"
+                 if world > 1 else "")
+              + f"), {head['reps']} timed reps after {args.warmup} warm-up; value = units x reps / summed rep time; "
+              "in place restored before every rep (outside the timing)")
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -311,7 +314,7 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "u16",
         "data": "synthetic",
-        "config": config_dict(args.config, head["units"], 1),
+        "config": config_dict(args.config, head["units"], world),
         "modes": {m: {"value": round(r["gbps"], 3), "best_gbps": round(r["gbps_best"], 3),
                       "ms_per_step": round(r["ms_per_rep"], 3), "reps": r["reps"]} for m, r in res.items()},
         "cpu_baseline": {"value": round(head["gbps"], 3), "unit": UNIT, "cores": head["cores"],

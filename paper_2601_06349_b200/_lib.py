@@ -184,7 +184,12 @@ def to_well_formed_part(x: torch.Tensor, out: Optional[torch.Tensor], part: int,
 
 def to_well_formed_batched(data: torch.Tensor, offsets: torch.Tensor, out: Optional[torch.Tensor] = None,
                            stream=None) -> torch.Tensor:
-    """Repair every string [offsets[s], offsets[s+1]) independently."""
+    """Repair every string [offsets[s], offsets[s+1]) independently.
+
+    Stream-ordered, no host sync. Units of `out` outside [offsets[0],
+    offsets[-1]) are not written: with out=None (a clone of `data`) they hold
+    the input, as in the host and C++ forms, which copy them; a caller-supplied
+    `out` keeps whatever it held there."""
     data = _units(data, "data")
     if not isinstance(offsets, torch.Tensor) and hasattr(offsets, "__dlpack__"):
         offsets = torch.from_dlpack(offsets)

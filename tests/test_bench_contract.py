@@ -53,3 +53,24 @@ def test_gpu_arm_contract(cuda):
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     ref = run_bench("--impl", "reference", "--steps", "2", "--warmup", "3", timeout=1200)
     assert ref["config"] == c
+
+
+def test_reference_arm_under_torchrun_env():
+    """Under torchrun (N>1) rank 0 alone runs the reference arm and prints the
+    same `config` the GPU arm prints at that world size; other ranks print
+    nothing and exit 0."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "2", "--warmup", "3", "--config", "c0"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["config"] == bench.config_dict("c0", 1 << 24, 2) and d["config"]["parallelism"] == "shard2"
+    env["RANK"] = env["LOCAL_RANK"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "2", "--warmup", "3", "--config", "c0"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0 and r.stdout.strip() == ""
