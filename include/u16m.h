@@ -146,8 +146,7 @@ u16m_status u16m_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
  * byte order (U16M_LITTLE_ENDIAN / U16M_BIG_ENDIAN) without a separate swap
  * pass, writing the same byte order, and ADDS the number of replaced units to
  * *replacements (device uint64; NULL = don't count). in/out: device, equal
- * (in place) or disjoint (an out at another 16-byte phase than in costs one
- * extra copy pass). Async. A BOM
+ * (in place) or disjoint, at any 2-byte alignment. Async. A BOM
  * (FEFF) is an ordinary non-surrogate unit and may stay in the buffer. */
 #define U16M_LITTLE_ENDIAN 0
 #define U16M_BIG_ENDIAN 1

@@ -265,13 +265,7 @@ u16m_status u16m_fix_utf16_bytes(const void* in, size_t n_units, void* out, int 
   if (o != i) U16M_TRY(check_device_ptr(out, "out"));
   if (replacements) U16M_TRY(check_device_ptr(replacements, "replacements"));
   const bool be = byte_order == U16M_BIG_ENDIAN;
-  if (i != o && ((reinterpret_cast<uintptr_t>(i) ^ reinterpret_cast<uintptr_t>(o)) & 15u)) {
-    // out at another 16-byte phase (rare for byte streams): copy the bytes
-    // across, then repair them in place — two passes, any alignment.
-    cudaError_t e = cudaMemcpyAsync(o, i, n_units * sizeof(uint16_t), cudaMemcpyDeviceToDevice, as_stream(stream));
-    if (e == cudaSuccess) e = u16m::launch_fix_bytes(o, n_units, o, be, replacements, as_stream(stream), -1, -1);
-    return e == cudaSuccess ? U16M_OK : cuda_fail(e, "codec repair (other-phase output)");
-  }
+  // (an out at another 16-byte phase runs the shifted-store form: one pass)
   const cudaError_t e = u16m::launch_fix_bytes(in, n_units, out, be, replacements, as_stream(stream), -1, -1);
   return e == cudaSuccess ? U16M_OK : cuda_fail(e, "codec repair kernel launch");
 }

@@ -40,6 +40,8 @@ struct Span;
 cudaError_t launch_stream(const Span& s, int part, cudaStream_t stream);
 // Copy into an `out` whose 16-byte phase differs from in's (s from make_span).
 cudaError_t launch_stream_shift(Span s, uint16_t* out, int part, cudaStream_t stream);
+cudaError_t launch_stream_shift_codec(const Span& s, uint16_t* out, bool big_endian, unsigned long long* count,
+                                      cudaStream_t stream);
 // Codec-fused form (u16m_stream.cu): same-phase buffers in little- or
 // big-endian byte order, optional device replacement counter (accumulated).
 cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long long* count, cudaStream_t stream);

@@ -444,7 +444,7 @@ cudaError_t launch_fix_bytes(const void* in, size_t n, void* out, bool big_endia
   const auto* i16 = static_cast<const uint16_t*>(in);
   auto* o16 = static_cast<uint16_t*>(out);
   const Span s = make_span(i16, n, o16, left, right, nullptr, nullptr, &same);
-  if (!(i16 == o16 || same)) return cudaErrorInvalidValue;
+  if (!(i16 == o16 || same)) return launch_stream_shift_codec(s, o16, big_endian, count, stream);
   return launch_stream_codec(s, big_endian, count, stream);
 }
 

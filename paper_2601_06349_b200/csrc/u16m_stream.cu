@@ -33,6 +33,22 @@ constexpr int kSThreads = 256;
 constexpr int kSWarpVecs = 32 * kSV;          // 256 vectors = 4 KiB per warp
 constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;  // 2048 vectors = 32 KiB per CTA
 
+// CTA-level sum of `counted` added to *count: one atomic per CTA (per-warp
+// atomics on one address serialise at the L2 slice). All threads call it.
+__device__ __forceinline__ void cta_count_add(uint32_t counted, unsigned long long* count) {
+  __shared__ uint32_t warp_counts[kSThreads / 32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) counted += __shfl_xor_sync(kFull, counted, o);
+  if ((threadIdx.x & 31) == 0) warp_counts[threadIdx.x / 32] = counted;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long c = 0;
+#pragma unroll
+    for (int w = 0; w < kSThreads / 32; w++) c += warp_counts[w];
+    if (c) atomicAdd(count, c);
+  }
+}
+
 // kBE: units are big-endian in memory (fused byte-order handling, §8(f-3));
 // kCount: add the number of rewritten units to *count (CTA reduction, one
 // atomic per CTA); kNoStore: validation only.
@@ -229,8 +245,10 @@ __device__ __forceinline__ uint4 shfl4(const uint4& v, int src, bool up) {
   return r;
 }
 
-template <int S>
-__global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int64_t q) {
+// kBE / kCount: the codec-fused forms (u16m_fix_utf16_bytes into an output at
+// another phase): big-endian units, rewritten units added to *count.
+template <int S, bool kBE = false, bool kCount = false>
+__global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int64_t q, unsigned long long* count) {
   const int lane = threadIdx.x & 31;
   const uint32_t lane_off = threadIdx.x / 32 * kSWarpVecs + lane;
   const uint64_t vbeg = s.lo / 8;
@@ -246,40 +264,47 @@ __global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int6
 
   uint4 v[kSV];
   uint32_t halo = 0;
+  uint32_t counted = 0;
   if (interior) {
     const uint4* src = s.in + v0;
 #pragma unroll
     for (int k = 0; k < kSV; k++) v[k] = ld_stream(src + k * 32);
     const uint16_t* src16 = reinterpret_cast<const uint16_t*>(src);
-    if (lane == 0) halo = src16[-1];
-    if (lane == 31) halo = src16[(kSV - 1) * 32 * 8 + 8];
+    if (lane == 0) halo = to_mem<kBE>(src16[-1]);
+    if (lane == 31) halo = to_mem<kBE>(src16[(kSV - 1) * 32 * 8 + 8]);
   } else {
 #pragma unroll
     for (int k = 0; k < kSV; k++) {
       const uint64_t vi = v0 + k * 32;
       v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
     }
+    // unit_at returns unit values for halos but raw memory words in range.
     const uint64_t warp_v0 = v0 - lane;
     if (lane == 0) {
       const int64_t a = static_cast<int64_t>(warp_v0 * 8) - 1;
       halo = unit_at(s, a);
+      if (a >= static_cast<int64_t>(s.lo)) halo = to_mem<kBE>(halo);
     }
-    if (lane == 31) halo = unit_at(s, static_cast<int64_t>((warp_v0 + kSWarpVecs) * 8));
+    if (lane == 31) {
+      const int64_t a = static_cast<int64_t>((warp_v0 + kSWarpVecs) * 8);
+      halo = unit_at(s, a);
+      if (a < static_cast<int64_t>(s.hi)) halo = to_mem<kBE>(halo);
+    }
 #pragma unroll
     for (int k = 0; k < kSV; k++) {
       const uint64_t vi = v0 + k * 32;
-      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, v[k]);
+      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges<kBE>(s, vi, v[k]);
     }
   }
 
-  Flags cur = classify8(v[0]);
+  Flags cur = classify8<kBE>(v[0]);
   uint32_t hp_carry = hflag_hi(halo);
   const uint32_t halo_l = lflag_lo(halo);
   uint4 carry = make_uint4(0, 0, 0, 0);  // lane 31's repaired vector k-1 (for lane 0)
 #pragma unroll
   for (int k = 0; k < kSV; k++) {
     Flags nxt;
-    if (k + 1 < kSV) nxt = classify8(v[k + 1]);
+    if (k + 1 < kSV) nxt = classify8<kBE>(v[k + 1]);
     const uint32_t up = __shfl_sync(kFull, cur.H1, (lane + 31) & 31);
     const uint32_t dn = __shfl_sync(kFull, cur.L0, (lane + 1) & 31);
     uint32_t ln = dn;
@@ -293,8 +318,13 @@ __global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int6
     hp_carry = up;
     uint32_t B0, B1;
     bad8(cur, hp, ln, B0, B1);
-    const uint4 r = blend(v[k], B0, B1);
+    const uint4 r = blend<kBE>(v[k], B0, B1);
     const uint64_t vi = v0 + k * 32;
+    if constexpr (kCount) {
+      uint32_t c0 = B0, c1 = B1;
+      if (!interior) mask_outside(s, vi, c0, c1);
+      if (vi < vend) counted += __popc(c0) + __popc(c1);
+    }
     if (interior) {
       uint4 prev = shfl4(r, 0, true);
       if (lane == 0) prev = carry;
@@ -319,6 +349,7 @@ __global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int6
     }
     if (k + 1 < kSV) cur = nxt;
   }
+  if constexpr (kCount) cta_count_add(counted, count);
 }
 
 // ---- batched form, non-persistent (buffer length known) ----------------------
@@ -781,7 +812,8 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
 }
 
 // Copy with out at a different 16-byte phase than in (see stream_shift_kernel).
-cudaError_t launch_stream_shift(Span s, uint16_t* out, int part, cudaStream_t stream) {
+template <bool kBE, bool kCount>
+static cudaError_t launch_shift_t(Span s, uint16_t* out, int part, unsigned long long* count, cudaStream_t stream) {
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
   const int64_t pi = static_cast<int64_t>(s.lo);  // in phase (units); s.lo == phase for a plain job
   const int64_t po = static_cast<int64_t>((oa & 15u) / 2);
@@ -799,17 +831,32 @@ cudaError_t launch_stream_shift(Span s, uint16_t* out, int part, cudaStream_t st
   if (grid == 0) return cudaSuccess;
   const unsigned g = static_cast<unsigned>(grid);
   switch (sh) {
-    case 1: stream_shift_kernel<1><<<g, kSThreads, 0, stream>>>(s, q); break;
-    case 2: stream_shift_kernel<2><<<g, kSThreads, 0, stream>>>(s, q); break;
-    case 3: stream_shift_kernel<3><<<g, kSThreads, 0, stream>>>(s, q); break;
-    case 4: stream_shift_kernel<4><<<g, kSThreads, 0, stream>>>(s, q); break;
-    case 5: stream_shift_kernel<5><<<g, kSThreads, 0, stream>>>(s, q); break;
-    case 6: stream_shift_kernel<6><<<g, kSThreads, 0, stream>>>(s, q); break;
-    case 7: stream_shift_kernel<7><<<g, kSThreads, 0, stream>>>(s, q); break;
+    case 1: stream_shift_kernel<1, kBE, kCount><<<g, kSThreads, 0, stream>>>(s, q, count); break;
+    case 2: stream_shift_kernel<2, kBE, kCount><<<g, kSThreads, 0, stream>>>(s, q, count); break;
+    case 3: stream_shift_kernel<3, kBE, kCount><<<g, kSThreads, 0, stream>>>(s, q, count); break;
+    case 4: stream_shift_kernel<4, kBE, kCount><<<g, kSThreads, 0, stream>>>(s, q, count); break;
+    case 5: stream_shift_kernel<5, kBE, kCount><<<g, kSThreads, 0, stream>>>(s, q, count); break;
+    case 6: stream_shift_kernel<6, kBE, kCount><<<g, kSThreads, 0, stream>>>(s, q, count); break;
+    case 7: stream_shift_kernel<7, kBE, kCount><<<g, kSThreads, 0, stream>>>(s, q, count); break;
     default: return cudaErrorInvalidValue;  // same phase: launch_stream
   }
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_stream_shift(Span s, uint16_t* out, int part, cudaStream_t stream) {
+  return launch_shift_t<false, false>(s, out, part, nullptr, stream);
+}
+
+// Codec-fused copy into an output at another 16-byte phase (byte order folded
+// into the gather, replacement count): one pass with shifted stores.
+cudaError_t launch_stream_shift_codec(const Span& s, uint16_t* out, bool big_endian, unsigned long long* count,
+                                      cudaStream_t stream) {
+  if (big_endian)
+    return count ? launch_shift_t<true, true>(s, out, kTilesAll, count, stream)
+                 : launch_shift_t<true, false>(s, out, kTilesAll, nullptr, stream);
+  return count ? launch_shift_t<false, true>(s, out, kTilesAll, count, stream)
+               : launch_shift_t<false, false>(s, out, kTilesAll, nullptr, stream);
 }
 
 // Byte swap of n units in place (p 16-byte aligned): the big-endian form of

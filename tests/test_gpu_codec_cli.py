@@ -174,17 +174,29 @@ def test_cli_layout_cases(tmp_path, cuda):
 
 
 def test_codec_other_phase_output(cuda):
-    """Byte-order-fused repair into an output at another 16-byte phase (copy,
-    then in place) — any alignment works, with the right replacement count."""
+    """Byte-order-fused repair into an output at another 16-byte phase
+    (shifted-store kernel, one pass) — every in/out phase pair, with and
+    without the replacement count; nothing outside the output is written."""
     x = np.frombuffer(P.generate_utf16le(100_003, 0.05, 0.02, 3), np.uint16)
     e = O.fix_scalar(x)
     for big in (False, True):
         raw = (x.astype(">u2") if big else x).view(np.uint16)
-        t = torch.from_numpy(raw.view(np.int16).copy()).cuda()
-        for po in (1, 3, 8):
-            base = torch.zeros(x.size + 16, dtype=torch.int16, device="cuda")
-            out = base[po:po + x.size]
-            got, cnt = P.to_well_formed_bytes(t, out=out, big_endian=big, count=True)
-            h = got.cpu().numpy().view(np.uint16)
-            h = h.view(">u2").astype(np.uint16) if big else h
-            assert (h == e).all() and cnt == int((x != e).sum()), (big, po)
+        src = torch.zeros(x.size + 16, dtype=torch.int16, device="cuda")
+        for pi in (0, 3):
+            t = src[pi:pi + x.size]
+            t.copy_(torch.from_numpy(raw.view(np.int16).copy()))
+            for po in range(8):
+                if po == pi:
+                    continue
+                base = torch.full((x.size + 16,), 0x5A5A, dtype=torch.int16, device="cuda")
+                out = base[po:po + x.size]
+                for count in (True, False):
+                    r = P.to_well_formed_bytes(t, out=out, big_endian=big, count=count)
+                    got, cnt = r if count else (r, None)
+                    h = got.cpu().numpy().view(np.uint16)
+                    h = h.view(">u2").astype(np.uint16) if big else h
+                    assert (h == e).all(), (big, pi, po, count)
+                    if count:
+                        assert cnt == int((x != e).sum()), (big, pi, po)
+                b = base.cpu().numpy()
+                assert (b[:po] == 0x5A5A).all() and (b[po + x.size:] == 0x5A5A).all(), (big, pi, po)
