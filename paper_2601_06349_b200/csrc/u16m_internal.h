@@ -24,8 +24,10 @@ cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_
 cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t num_strings,
                            uint16_t* out, cudaStream_t stream);
 
+// In-place write-back granularity in lanes of 16 B: 2 = one 32-byte DRAM
+// sector (measured best of 16/32/64/128 B; the former U16M_GRAN A/B knob,
+// profiles/README.md — scripts/ab_lib.sh rebuilds an older commit to rerun it).
 constexpr int kDefaultInplaceGran = 2;
-int inplace_granularity();
 
 // Part of a job: part = 0 all tiles, 1 only the two edge tiles (the only
 // ones that read the halos), 2 only the interior tiles. Edges + interior ==

@@ -391,16 +391,6 @@ static int kernel_choice() {
   return choice;
 }
 
-// In-place write-back granularity in lanes of 16 B (U16M_GRAN: 1, 2, 4, 8).
-int inplace_granularity() {
-  static const int g = [] {
-    const char* e = std::getenv("U16M_GRAN");
-    const int v = e ? std::atoi(e) : kDefaultInplaceGran;
-    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : kDefaultInplaceGran;
-  }();
-  return g;
-}
-
 template <int kGran>
 static cudaError_t launch_inplace(const Span& s, uint64_t grid, cudaStream_t stream) {
   return launch<kInPlace, true, false, kGran>(s, kNoBatch, kNoScan, grid, stream);
@@ -425,14 +415,7 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
   const uint64_t grid = part == kTilesAll ? ntiles
                         : part == kTilesEdges ? (ntiles < 2 ? ntiles : 2)
                                               : (ntiles > 2 ? ntiles - 2 : 0);
-  if (in == out) {
-    switch (inplace_granularity()) {
-      case 1: return launch_inplace<1>(s, grid, stream);
-      case 4: return launch_inplace<4>(s, grid, stream);
-      case 8: return launch_inplace<8>(s, grid, stream);
-      default: return launch_inplace<2>(s, grid, stream);
-    }
-  }
+  if (in == out) return launch_inplace<kDefaultInplaceGran>(s, grid, stream);
   if (same) return launch<kCopy, true, false>(s, kNoBatch, kNoScan, grid, stream);
   return launch<kCopy, false, false>(s, kNoBatch, kNoScan, grid, stream);
 }

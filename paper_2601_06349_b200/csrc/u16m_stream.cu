@@ -699,10 +699,9 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
     }
   } else if (in != out) {
     e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<false, 1>, s, offsets, cnt, ph, tab, nwt, nn, q0);
-  } else if (inplace_granularity() == 1) {
-    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, 1>, s, offsets, cnt, ph, tab, nwt, nn, q0);
   } else {
-    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, 2>, s, offsets, cnt, ph, tab, nwt, nn, q0);
+    e = cudaLaunchKernelEx(&cfg, batched_tile_kernel<true, kDefaultInplaceGran>, s, offsets, cnt, ph, tab, nwt, nn,
+                           q0);
   }
   if (e != cudaSuccess) return e;
   note_launch();
@@ -742,12 +741,7 @@ static cudaError_t launch_stream_v(Span s, int part, cudaStream_t stream) {
   if (s.in != s.out) {
     stream_kernel<false, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr);
   } else {
-    switch (inplace_granularity()) {
-      case 1: stream_kernel<true, 1, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr); break;
-      case 4: stream_kernel<true, 4, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr); break;
-      case 8: stream_kernel<true, 8, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr); break;
-      default: stream_kernel<true, 2, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr); break;
-    }
+    stream_kernel<true, kDefaultInplaceGran, kV, kMB><<<g, kSThreads, 0, stream>>>(s, nullptr, nullptr);
   }
   note_launch();
   return cudaGetLastError();

@@ -347,12 +347,7 @@ cudaError_t launch_repair_tma(const uint16_t* in, size_t n, uint16_t* out, int32
   const uint64_t ntiles = ((s.hi + 7) / 8 - s.lo / 8 + kCtaVecs - 1) / kCtaVecs;
   const tma::BatchArgsT b{nullptr, 0, 0};
   if (in != out) return tma::launch_tma<0, false, 1>(s, b, ntiles, stream);
-  switch (inplace_granularity()) {
-    case 1: return tma::launch_tma<1, false, 1>(s, b, ntiles, stream);
-    case 2: return tma::launch_tma<1, false, 2>(s, b, ntiles, stream);
-    case 8: return tma::launch_tma<1, false, 8>(s, b, ntiles, stream);
-    default: return tma::launch_tma<1, false, 4>(s, b, ntiles, stream);
-  }
+  return tma::launch_tma<1, false, kDefaultInplaceGran>(s, b, ntiles, stream);
 }
 
 cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of kernel knobs on one config: VARIANTS is a list of "NAME=VALUE[,NAME=VALUE]" (or "base").
-# Usage: CFG=c1 VARIANTS="base U16M_GRAN=4" bash scripts/ab_env.sh
+# Usage: CFG=c1 VARIANTS="base U16M_PREFETCH=0" bash scripts/ab_env.sh
 mkdir -p gpurun_out
 for rep in $(seq ${REPS:-2}); do
   for v in ${VARIANTS:-base}; do

@@ -13,13 +13,9 @@ VARIANTS = [
     {},
     {"U16M_KERNEL": "tma"},
     {"U16M_KERNEL": "general"},
-    {"U16M_KERNEL": "tma", "U16M_GRAN": "1"},
-    {"U16M_GRAN": "1"},
-    {"U16M_GRAN": "4"},
-    {"U16M_GRAN": "8"},
     {"U16M_KERNEL": "ldg"},
-    {"U16M_KERNEL": "ldg", "U16M_GRAN": "1"},
-    {"U16M_GRAN": "4", "U16M_PIPE_CHUNK_KIB": "64"},
+    {"U16M_PREFETCH": "0"},
+    {"U16M_BATCHED_PDL": "0"},
     {"U16M_PIPE_CHUNK_KIB": "64", "U16M_HOST_THREADS": "3"},
 ]
 
