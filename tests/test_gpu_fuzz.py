@@ -68,6 +68,17 @@ def test_fuzz_all_entry_points(P, cuda):
             bt = dev(x.astype(">u2").view(np.uint16))
             ob, c = P.to_well_formed_bytes(bt, big_endian=True, count=True)
             assert (host(ob).view(">u2").astype(np.uint16) == e0).all() and c == int((x != e0).sum()), it
+            # the same between arbitrary 16-byte phases (shifted-store codec kernel), LE and BE
+            big = bool(it & 1)
+            sb = arena[pi:pi + n]
+            sb.copy_(bt if big else dev(x))
+            ob2 = arena2[po:po + n]
+            r = P.to_well_formed_bytes(sb, out=ob2, big_endian=big, count=bool(it & 2))
+            hb = host(ob2)
+            hb = hb.view(">u2").astype(np.uint16) if big else hb
+            assert (hb == e0).all(), ("codec phases", it, n, pi, po, big)
+            if it & 2:
+                assert r[1] == int((x != e0).sum()), ("codec phases count", it)
         # batched over a random split of x
         cuts = np.sort(rng.integers(0, n + 1, int(rng.integers(0, 40))))
         offs = np.concatenate([[int(rng.integers(0, min(n, 5) + 1))] if n else [0], cuts, [n]]).astype(np.int64)
