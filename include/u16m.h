@@ -105,7 +105,9 @@ u16m_status u16m_to_well_formed_part(const uint16_t* in, size_t n, uint16_t* out
  * device device_ids[g]; shard_out[g] == shard_in[g] for in-place. Halo units
  * cross shard edges as direct peer loads over NVLink when peer access is
  * available, else through a 2-byte peer copy. Synchronous: returns when every
- * shard is repaired. Device ids may repeat (virtual shards on one GPU). */
+ * shard is repaired. Runs on the library's own non-blocking streams, so work
+ * that wrote the shards must be complete (synchronised) before the call.
+ * Device ids may repeat (virtual shards on one GPU). */
 u16m_status u16m_to_well_formed_sharded(int num_shards, const int* device_ids,
                                         const uint16_t* const* shard_in, const size_t* shard_len,
                                         uint16_t* const* shard_out);
