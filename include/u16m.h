@@ -161,6 +161,13 @@ u16m_status u16m_fix_utf16_bytes(const void* in, size_t n_units, void* out, int 
  * order; up to `limit` offsets, number written in *count_out). */
 u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out, int byte_order,
                                       unsigned long long* replacements);
+/* The same spread over several GPUs as u16m_to_well_formed_host_multi
+ * (u16m_fix_utf16_bytes_host = every visible device): contiguous ranges, one
+ * per device and PCIe link, halo units read from the caller's input in its
+ * byte order; *replacements is the sum over the ranges. */
+u16m_status u16m_fix_utf16_bytes_host_multi(const void* in, size_t n_units, void* out, int byte_order,
+                                            unsigned long long* replacements, int num_devices,
+                                            const int* device_ids);
 u16m_status u16m_unpaired_offsets_host(const uint16_t* in, size_t n, size_t limit,
                                        unsigned long long* offsets_out, size_t* count_out);
 /* Same over raw UTF-16 bytes in the given byte order (CLI `check` of a

@@ -75,6 +75,9 @@ _L.u16m_select_kernel.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _sz]
 _L.u16m_select_kernel.restype = _st
 _L.u16m_to_well_formed_host_multi.argtypes = [_u16p, _sz, _u16p, ctypes.c_int, _vp]
 _L.u16m_to_well_formed_host_multi.restype = _st
+_L.u16m_fix_utf16_bytes_host_multi.argtypes = [_vp, _sz, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong),
+                                               ctypes.c_int, _vp]
+_L.u16m_fix_utf16_bytes_host_multi.restype = _st
 
 
 class U16MError(RuntimeError):
@@ -398,7 +401,8 @@ def generate_utf16le(units: int, pair_pct: float = 0.0, mismatch_pct: float = 0.
 def fix_utf16_bytes(data, byte_order: str = "le") -> tuple[bytes, int]:
     """§8(f-3) codec fusion: repair raw UTF-16 bytes in their own byte order
     ("le" / "be") on the GPU without a swap pass; returns (bytes, number of
-    replaced units). The CLI `fix` path (paper_2601_06349_b200/u16m)."""
+    replaced units). The CLI `fix` path (paper_2601_06349_b200/u16m); large
+    inputs are spread over every visible GPU."""
     mv = _check_bytes(data)
     if byte_order not in ("le", "be"):
         raise ValueError("byte_order must be 'le' or 'be'")

@@ -515,12 +515,25 @@ u16m_status u16m_to_well_formed_host_multi(const uint16_t* in, size_t n, uint16_
   return host_pipeline(in, n, out, -1, nullptr, &devs);
 }
 
-u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out, int byte_order,
-                                      unsigned long long* replacements) {
+u16m_status u16m_fix_utf16_bytes_host_multi(const void* in, size_t n_units, void* out, int byte_order,
+                                            unsigned long long* replacements, int num_devices,
+                                            const int* device_ids) {
   if (byte_order != U16M_LITTLE_ENDIAN && byte_order != U16M_BIG_ENDIAN)
     return fail(U16M_ERR_INVALID_ARGUMENT, "byte_order must be U16M_LITTLE_ENDIAN or U16M_BIG_ENDIAN");
-  return host_pipeline(static_cast<const uint16_t*>(in), n_units, static_cast<uint16_t*>(out), byte_order,
-                       replacements);
+  const auto* i = static_cast<const uint16_t*>(in);
+  auto* o = static_cast<uint16_t*>(out);
+  U16M_TRY(check_pair(i, n_units, o));
+  if (replacements) *replacements = 0;
+  if (n_units == 0) return U16M_OK;
+  std::vector<int> devs;
+  U16M_TRY(device_list(num_devices, device_ids, &devs));
+  return host_pipeline(i, n_units, o, byte_order, replacements, &devs);
+}
+
+u16m_status u16m_fix_utf16_bytes_host(const void* in, size_t n_units, void* out, int byte_order,
+                                      unsigned long long* replacements) {
+  // every visible GPU, each over its own PCIe link (one for jobs under 64 Mi units)
+  return u16m_fix_utf16_bytes_host_multi(in, n_units, out, byte_order, replacements, 0, nullptr);
 }
 
 u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units, const int64_t* offsets,

@@ -133,3 +133,31 @@ def test_sharded_over_distinct_devices(P, cuda):
     out = torch.empty_like(pin).pin_memory()
     assert _multi(P, pin.data_ptr(), n, out.data_ptr(), tuple(devs)) == 0
     assert (out.numpy().view(np.uint16) == e).all()
+
+
+@pytest.mark.parametrize("big", [False, True])
+def test_codec_host_multi_ranges(P, cuda, big):
+    """Byte-order-fused host repair over several (virtual) devices: every
+    range edge reads its halo units from host memory in the job's byte order,
+    and the replacement count is the sum over the ranges."""
+    n = 3 * (1 << 25) + 4097  # three ranges of >= 32 Mi units, ragged
+    x = O.gen_config(4, n, seed=31, shard_len=n // 3)
+    e = O.stencil_mt(x)
+    raw = (x.astype(">u2") if big else x).view(np.uint16)
+    hin = torch.from_numpy(raw.view(np.int16).copy()).pin_memory()
+    hout = torch.empty(n, dtype=torch.int16, pin_memory=True)
+    L = P._lib.raw()
+    cnt = ctypes.c_ulonglong(0)
+    for ids in ((0, 0, 0), (0, 0)):
+        assert L.u16m_fix_utf16_bytes_host_multi(hin.data_ptr(), n, hout.data_ptr(), int(big), ctypes.byref(cnt),
+                                                 len(ids), _ids(*ids)) == 0
+        h = hout.numpy().view(np.uint16)
+        h = h.view(">u2").astype(np.uint16) if big else h
+        assert np.array_equal(h, e) and cnt.value == int((x != e).sum()), ids
+    # pageable input, in place
+    buf = raw.copy()
+    assert L.u16m_fix_utf16_bytes_host_multi(buf.ctypes.data, n, buf.ctypes.data, int(big), ctypes.byref(cnt), 3,
+                                             _ids(0, 0, 0)) == 0
+    h = buf.view(">u2").astype(np.uint16) if big else buf
+    assert np.array_equal(h, e) and cnt.value == int((x != e).sum())
+    assert L.u16m_fix_utf16_bytes_host_multi(hin.data_ptr(), n, hout.data_ptr(), 2, None, 1, _ids(0)) == 1
