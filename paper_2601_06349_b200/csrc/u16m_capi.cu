@@ -78,23 +78,39 @@ namespace u16m {
 
 // Units from `p` to the end of the device allocation holding it (driver
 // cuMemGetAddressRange through the runtime's entry-point query, so the
-// library needs no libcuda link), 0 when unknown.
+// library needs no libcuda link), 0 when unknown. Memory mapped through the
+// virtual memory management API (cuMemCreate + cuMemMap: e.g. PyTorch's
+// expandable segments) is "unknown": there the range is one physical mapping
+// (a 20 MiB page), not the buffer, and a tensor spans many of them
+// (scripts/addr_range_probe.py: 2.9 M wrong units before this check).
+// cuMemRetainAllocationHandle succeeds exactly for such mappings (it fails
+// for cudaMalloc and stream-ordered pool allocations, whose range is the
+// whole allocation).
 size_t allocation_units_after(const void* p) {
-  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
-  static Fn fn = [] {
+  using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  using RetainFn = CUresult (*)(CUmemGenericAllocationHandle*, void*);
+  using ReleaseFn = CUresult (*)(CUmemGenericAllocationHandle);
+  auto entry = [](const char* name) -> void* {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess) {
+    if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
       cudaGetLastError();
-      return Fn(nullptr);
+      return nullptr;
     }
-    return reinterpret_cast<Fn>(f);
-  }();
-  if (fn == nullptr || p == nullptr) return 0;
+    return f;
+  };
+  static RangeFn range = reinterpret_cast<RangeFn>(entry("cuMemGetAddressRange"));
+  static RetainFn retain = reinterpret_cast<RetainFn>(entry("cuMemRetainAllocationHandle"));
+  static ReleaseFn release = reinterpret_cast<ReleaseFn>(entry("cuMemRelease"));
+  if (range == nullptr || retain == nullptr || release == nullptr || p == nullptr) return 0;
+  CUmemGenericAllocationHandle h = 0;
+  if (retain(&h, const_cast<void*>(p)) == CUDA_SUCCESS) {
+    release(h);
+    return 0;  // VMM mapping: the range is not a bound of the buffer
+  }
   CUdeviceptr base = 0;
   size_t size = 0;
-  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return 0;
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
   if (a < base || a >= base + size) return 0;
   return (base + size - a) / sizeof(uint16_t);
@@ -239,10 +255,11 @@ u16m_status u16m_to_well_formed_batched(const uint16_t* in, const int64_t* offse
   // a host sync. The allocations holding `in` and `out` bound it instead
   // (cuMemGetAddressRange): the register-staged tile kernel of the
   // length-aware form runs with its grid sized from that bound (CTAs past
-  // offsets[S] exit at once). When the bound is unknown (not a cudaMalloc'd
-  // range) or loose enough that idle CTAs could cost more than the tile form
-  // saves (> 4 GiB past `in`), the persistent TMA kernel runs instead: its
-  // grid is the SM count and it reads the range on the device.
+  // offsets[S] exit at once). When the bound is unknown (not a cudaMalloc'd or
+  // pool range, e.g. VMM-mapped pages) or loose enough that idle CTAs could
+  // cost more than the tile form saves (> 4 GiB past `in`), the persistent TMA
+  // kernel runs instead: its grid is the SM count and it reads the range on
+  // the device, so it needs no bound at all.
   const size_t bound = std::min(u16m::allocation_units_after(in), u16m::allocation_units_after(out));
   cudaError_t e;
   if (bound > 0 && bound <= (size_t(1) << 31) && u16m::batched_tiles_enabled())

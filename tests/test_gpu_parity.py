@@ -1,5 +1,6 @@
 """GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle
 and the reference's golden vectors. Bit-exact everywhere (integer path)."""
+import os
 import numpy as np
 import pytest
 import torch
@@ -753,3 +754,17 @@ def test_python_batch_api(P, cuda):
     texts = ["ok", "", "a\ud800", "\udc00b", "\U0001F60A", "x😊y"]
     assert P.fix_str_batch(texts) == [P.fix_str(t) for t in texts]
     assert P.fix_utf16le_batch([]) == [] and P.fix_utf16le_batch([b"", b""]) == [b"", b""]
+
+
+@pytest.mark.parametrize("conf", ["", "expandable_segments:True", "backend:cudaMallocAsync"])
+def test_lengthless_entry_under_every_torch_allocator(cuda, conf):
+    """The length-less batched entry sizes its grid from the allocation holding
+    the strings; with VMM-mapped memory (expandable segments) that range is one
+    20 MiB page, so it must take the bound-free kernel — exact either way."""
+    import subprocess
+    import sys
+
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gpu_helpers", "lengthless_check.py")
+    env = dict(os.environ, PYTORCH_CUDA_ALLOC_CONF=conf)
+    r = subprocess.run([sys.executable, helper], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
