@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 
 def dev(x):
-    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint16).view(np.int16)).cuda()
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint16).view(np.int16).copy()).cuda()
 
 
 def host(t):
@@ -768,3 +768,44 @@ def test_lengthless_entry_under_every_torch_allocator(cuda, conf):
     env = dict(os.environ, PYTORCH_CUDA_ALLOC_CONF=conf)
     r = subprocess.run([sys.executable, helper], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_concurrent_callers_on_their_own_streams(P, cuda):
+    """SURVEY.md §8(b) threading contract: the library is re-entrant — host
+    threads repairing on their own streams (device API) and through the host
+    pipeline at the same time all get exact results."""
+    import threading
+
+    rng = np.random.default_rng(77)
+    jobs = [rng.integers(0, 65536, int(rng.integers(1, 3_000_000))).astype(np.uint16) for _ in range(8)]
+    exp = [O.stencil(x) for x in jobs]
+    errors = []
+
+    def device_worker(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(5):
+                    t = torch.from_numpy(jobs[k].view(np.int16).copy()).cuda(non_blocking=False)
+                    y = P.to_well_formed(t, stream=s)
+                    P.to_well_formed_(t, stream=s)
+                    s.synchronize()
+                    assert (y.cpu().numpy().view(np.uint16) == exp[k]).all()
+                    assert (t.cpu().numpy().view(np.uint16) == exp[k]).all()
+        except Exception as e:  # noqa: BLE001
+            errors.append((k, repr(e)))
+
+    def host_worker(k):
+        try:
+            for _ in range(5):
+                got = np.frombuffer(P.fix_utf16le(jobs[k].tobytes()), np.uint16)
+                assert (got == exp[k]).all()
+        except Exception as e:  # noqa: BLE001
+            errors.append((k, repr(e)))
+
+    threads = [threading.Thread(target=device_worker if k % 2 else host_worker, args=(k,)) for k in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
