@@ -797,9 +797,12 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int pf = prefetch_setting();
-    s.prefetch_tiles = pf >= 0 ? pf : (ntiles > static_cast<uint64_t>(2 * sms * 4) ? sms * 4 : 0);
+    s.prefetch_tiles = pf >= 0 ? pf : (ntiles > static_cast<uint64_t>(2 * sms * 5) ? sms * 5 : 0);
   }
-  stream_kernel<false, 1, 8, 4, false, true, true>
+  // 5 resident CTAs per SM (48 registers, 16-20 bytes of spills): without
+  // stores the extra CTA's loads in flight win (C1 98.3 -> 96.3 us, C4 1378 ->
+  // 1344 us, profiles/r02/count_probe.txt); 6 spill 2 KB and 4 is slower.
+  stream_kernel<false, 1, 8, 5, false, true, true>
       <<<static_cast<unsigned>(ntiles), kSThreads, 0, stream>>>(s, count, half_tile_counts);
   note_launch();
   return cudaGetLastError();
