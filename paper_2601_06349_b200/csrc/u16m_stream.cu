@@ -157,9 +157,13 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
     const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
     const uint64_t vi = v0 + k * 32;
     if constexpr (kCount) {
-      uint32_t c0 = B0, c1 = B1;
-      if (!interior) mask_outside(s, vi, c0, c1);
-      if (vi < vend) counted += __popc(c0) + __popc(c1);
+      if (interior) {  // every unit of the vector is in range: no per-vector bounds test
+        counted += __popc(B0) + __popc(B1);
+      } else {
+        uint32_t c0 = B0, c1 = B1;
+        mask_outside(s, vi, c0, c1);
+        if (vi < vend) counted += __popc(c0) + __popc(c1);
+      }
     }
     if (kNoStore) {
       // validation only (count)
@@ -321,9 +325,13 @@ __global__ void __launch_bounds__(kSThreads, 4) stream_shift_kernel(Span s, int6
     const uint4 r = blend<kBE>(v[k], B0, B1);
     const uint64_t vi = v0 + k * 32;
     if constexpr (kCount) {
-      uint32_t c0 = B0, c1 = B1;
-      if (!interior) mask_outside(s, vi, c0, c1);
-      if (vi < vend) counted += __popc(c0) + __popc(c1);
+      if (interior) {
+        counted += __popc(B0) + __popc(B1);
+      } else {
+        uint32_t c0 = B0, c1 = B1;
+        mask_outside(s, vi, c0, c1);
+        if (vi < vend) counted += __popc(c0) + __popc(c1);
+      }
     }
     if (interior) {
       uint4 prev = shfl4(r, 0, true);
