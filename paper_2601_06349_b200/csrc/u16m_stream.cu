@@ -49,53 +49,22 @@ __device__ __forceinline__ void cta_count_add(uint32_t counted, unsigned long lo
   }
 }
 
-// kBE: units are big-endian in memory (fused byte-order handling, §8(f-3));
-// kCount: add the number of rewritten units to *count (CTA reduction, one
-// atomic per CTA); kNoStore: validation only.
-template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false,
-          bool kNoStore = false>
-__global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count,
-                                                                      uint32_t* half_tile_counts) {
-  // validation: the offsets scan's prefix kernel is a programmatic dependent
-  if constexpr (kCount && kNoStore) asm volatile("griddepcontrol.launch_dependents;");
+// One tile of the stream kernel. kEdge = false: every vector of the tile lies
+// inside [lo, hi) (the hot path: no per-vector range tests, 128-bit stores
+// only; the warp tile's outer halo unit is the only thing that may come from
+// the halo rule). kEdge = true: the first / last tile of a job, with range
+// patches and per-unit stores for vectors that straddle [lo, hi). Two
+// separate bodies so that none of the edge bookkeeping is computed on the
+// hot path (it was hoisted into it when both shared one loop: ~20 extra
+// instructions per vector).
+template <bool kEdge, bool kInPlace, int kGran, int kSV, bool kBE, bool kCount, bool kNoStore>
+__device__ __forceinline__ void stream_tile(const Span& s, uint64_t tv0, uint64_t vend, int lane,
+                                            uint32_t lane_off, uint32_t& counted) {
   constexpr int kSWarpVecs = 32 * kSV;
-  constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
-  const int lane = threadIdx.x & 31;
-  const uint32_t lane_off = threadIdx.x / 32 * kSWarpVecs + lane;
-  const uint64_t vbeg = s.lo / 8;
-  const uint64_t vend = (s.hi + 7) / 8;
-  const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
-  uint64_t nwork = ntiles;
-  if (s.tile_sel == kTilesEdges) nwork = ntiles < 2 ? ntiles : 2;
-  if (s.tile_sel == kTilesInterior) nwork = ntiles > 2 ? ntiles - 2 : 0;
-  uint32_t counted = 0;
-  uint64_t count_tile = 0;
-  // One tile per CTA (persistent grids measured 15-20 % slower: profiles/README.md).
-  for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-  // The last tile goes first: a ragged last tile runs the edge code path
-  // (range patches, per-unit stores), whose cold instruction fetch made it
-  // finish ~14 us after everything else when it was dispatched last.
-  uint64_t tile = w == 0 ? ntiles - 1 : w - 1;
-  if (s.tile_sel == kTilesEdges) tile = w == 0 ? 0 : ntiles - 1;
-  if (s.tile_sel == kTilesInterior) tile = w + 1;
-  count_tile = tile;
-  const uint64_t tv0 = vbeg + tile * kSCtaVecs;
-  // "interior": every vector of the tile lies fully inside [lo, hi) — also the
-  // first and last tile of a job whose ends are 16-byte aligned; only their
-  // outer halo units come from the halo rule instead of memory.
-  const bool interior = tv0 * 8 >= s.lo && (tv0 + kSCtaVecs) * 8 <= s.hi;
   const uint64_t v0 = tv0 + lane_off;  // this lane's vector k sits at v0 + 32k
-
   uint4 v[kSV];
   uint32_t halo = 0;
-  if (s.prefetch_tiles > 0 && threadIdx.x == 0) {
-    // One bulk L2 prefetch of the tile a later wave of CTAs will stream: extra
-    // bytes in flight without registers (TMA prefetch, no smem, no barrier).
-    const uint64_t pv = tv0 + static_cast<uint64_t>(s.prefetch_tiles) * kSCtaVecs;
-    if (pv + kSCtaVecs <= vend)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s.in + pv), "r"(kSCtaVecs * 16) : "memory");
-  }
-  if (interior) {
+  if constexpr (!kEdge) {
     const uint4* src = s.in + v0;
 #pragma unroll
     for (int k = 0; k < kSV; k++) v[k] = ld_stream(src + k * 32);
@@ -136,16 +105,17 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
   Flags cur = classify8<kBE>(v[0]);
   uint32_t hp_carry = hflag_hi(halo);  // lane 0: H flags of the unit before vector 0
   const uint32_t halo_l = lflag_lo(halo);
+  const int up_lane = (lane + 31) & 31, dn_lane = (lane + 1) & 31;
   uint4* dst = s.out + v0;
 #pragma unroll
   for (int k = 0; k < kSV; k++) {
     Flags nxt;
     if (k + 1 < kSV) nxt = classify8<kBE>(v[k + 1]);
-    const uint32_t up = __shfl_sync(kFull, cur.H1, (lane + 31) & 31);  // lane 0 gets lane 31's (vector k)
-    const uint32_t dn = __shfl_sync(kFull, cur.L0, (lane + 1) & 31);
+    const uint32_t up = __shfl_sync(kFull, cur.H1, up_lane);  // lane 0 gets lane 31's (vector k)
+    const uint32_t dn = __shfl_sync(kFull, cur.L0, dn_lane);
     uint32_t ln = dn;
     if (k + 1 < kSV) {
-      const uint32_t dn_next = __shfl_sync(kFull, nxt.L0, (lane + 1) & 31);  // lane 31 gets lane 0's (vector k+1)
+      const uint32_t dn_next = __shfl_sync(kFull, nxt.L0, dn_lane);  // lane 31 gets lane 0's (vector k+1)
       if (lane == 31) ln = dn_next;
     } else if (lane == 31) {
       ln = halo_l;
@@ -155,33 +125,83 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
     uint32_t B0, B1;
     bad8(cur, hp, ln, B0, B1);
     const bool store = kInPlace ? group_dirty<kGran>((B0 | B1) != 0, lane) : true;
-    const uint64_t vi = v0 + k * 32;
-    if constexpr (kCount) {
-      if (interior) {  // every unit of the vector is in range: no per-vector bounds test
-        counted += __popc(B0) + __popc(B1);
-      } else {
+    if constexpr (!kEdge) {
+      if constexpr (kCount) counted += __popc(B0) + __popc(B1);
+      if constexpr (!kNoStore) {
+        if (store) st_stream(dst + k * 32, blend<kBE>(v[k], B0, B1));
+      }
+    } else {
+      const uint64_t vi = v0 + k * 32;
+      if constexpr (kCount) {
         uint32_t c0 = B0, c1 = B1;
         mask_outside(s, vi, c0, c1);
         if (vi < vend) counted += __popc(c0) + __popc(c1);
       }
-    }
-    if (kNoStore) {
-      // validation only (count)
-    } else if (interior || (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi)) {
-      if (store) st_stream(dst + k * 32, blend<kBE>(v[k], B0, B1));
-    } else if (store && vi < vend) {
-      const uint4 r = blend<kBE>(v[k], B0, B1);
+      if constexpr (!kNoStore) {
+        if (vi * 8 >= s.lo && vi * 8 + 8 <= s.hi) {
+          if (store) st_stream(dst + k * 32, blend<kBE>(v[k], B0, B1));
+        } else if (store && vi < vend) {
+          const uint4 r = blend<kBE>(v[k], B0, B1);
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const uint64_t a = vi * 8 + j;
-        if (a >= s.lo && a < s.hi) {
-          const uint32_t u = get_unit(r, j);
-          if (!kInPlace || u != get_unit(v[k], j)) s.out_units[a - s.lo] = static_cast<uint16_t>(u);
+          for (int j = 0; j < 8; j++) {
+            const uint64_t a = vi * 8 + j;
+            if (a >= s.lo && a < s.hi) {
+              const uint32_t u = get_unit(r, j);
+              if (!kInPlace || u != get_unit(v[k], j)) s.out_units[a - s.lo] = static_cast<uint16_t>(u);
+            }
+          }
         }
       }
     }
     if (k + 1 < kSV) cur = nxt;
   }
+}
+
+// kBE: units are big-endian in memory (fused byte-order handling, §8(f-3));
+// kCount: add the number of rewritten units to *count (CTA reduction, one
+// atomic per CTA); kNoStore: validation only.
+template <bool kInPlace, int kGran, int kSV = 8, int kMinBlocks = 4, bool kBE = false, bool kCount = false,
+          bool kNoStore = false>
+__global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, unsigned long long* count,
+                                                                      uint32_t* half_tile_counts) {
+  // validation: the offsets scan's prefix kernel is a programmatic dependent
+  if constexpr (kCount && kNoStore) asm volatile("griddepcontrol.launch_dependents;");
+  constexpr int kSWarpVecs = 32 * kSV;
+  constexpr int kSCtaVecs = (kSThreads / 32) * kSWarpVecs;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lane_off = threadIdx.x / 32 * kSWarpVecs + lane;
+  const uint64_t vbeg = s.lo / 8;
+  const uint64_t vend = (s.hi + 7) / 8;
+  const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
+  uint64_t nwork = ntiles;
+  if (s.tile_sel == kTilesEdges) nwork = ntiles < 2 ? ntiles : 2;
+  if (s.tile_sel == kTilesInterior) nwork = ntiles > 2 ? ntiles - 2 : 0;
+  uint32_t counted = 0;
+  uint64_t count_tile = 0;
+  // One tile per CTA (persistent grids measured 15-20 % slower: profiles/README.md).
+  for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    // The last tile goes first: a ragged last tile runs the edge code path
+    // (range patches, per-unit stores), whose cold instruction fetch made it
+    // finish ~14 us after everything else when it was dispatched last.
+    uint64_t tile = w == 0 ? ntiles - 1 : w - 1;
+    if (s.tile_sel == kTilesEdges) tile = w == 0 ? 0 : ntiles - 1;
+    if (s.tile_sel == kTilesInterior) tile = w + 1;
+    count_tile = tile;
+    const uint64_t tv0 = vbeg + tile * kSCtaVecs;
+    if (s.prefetch_tiles > 0 && threadIdx.x == 0) {
+      // One bulk L2 prefetch of the tile a later wave of CTAs will stream: extra
+      // bytes in flight without registers (TMA prefetch, no smem, no barrier).
+      const uint64_t pv = tv0 + static_cast<uint64_t>(s.prefetch_tiles) * kSCtaVecs;
+      if (pv + kSCtaVecs <= vend)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s.in + pv), "r"(kSCtaVecs * 16) : "memory");
+    }
+    // "interior": every vector of the tile lies fully inside [lo, hi) — also the
+    // first and last tile of a job whose ends are 16-byte aligned; only their
+    // outer halo units come from the halo rule instead of memory.
+    if (tv0 * 8 >= s.lo && (tv0 + kSCtaVecs) * 8 <= s.hi)
+      stream_tile<false, kInPlace, kGran, kSV, kBE, kCount, kNoStore>(s, tv0, vend, lane, lane_off, counted);
+    else
+      stream_tile<true, kInPlace, kGran, kSV, kBE, kCount, kNoStore>(s, tv0, vend, lane, lane_off, counted);
   }  // tile loop
   if constexpr (kCount) {
     // CTA-level reduction, one atomic per CTA (per-warp atomics on one
