@@ -56,8 +56,16 @@ struct HostPipe {
   cudaEvent_t loaded[kRing] = {}, repaired[kRing] = {}, drained[kRing] = {};
   uint16_t* stage[kStage] = {};           // pinned, allocated on the first pageable job
   cudaEvent_t staged[kStage] = {};
+  uint16_t* small = nullptr;              // pinned + mapped, small jobs (kSmallUnits), lazily
+  unsigned long long* small_count = nullptr;  // pinned, the small path's count read-back
   std::mutex mu;                          // one job per device pipeline at a time
 };
+
+// Jobs up to this many units skip the copy-engine pipeline: the kernel reads
+// and writes host memory directly over PCIe (pinned memory is mapped into the
+// device's address space), so a call is one launch + one synchronisation
+// instead of two DMAs, four events and three synchronisations.
+constexpr size_t kSmallUnits = size_t(64) << 10;
 
 // Streaming (non-temporal) copy for the staging copies: the destination is
 // written once and read next by a DMA engine or not at all, so bypassing the
@@ -406,6 +414,64 @@ u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out,
 
 // One device's whole share of a host job: select the device on this thread,
 // take its pipeline, reset its counter, run the range, read the count back.
+// Device-accessible address of pinned (page-locked, mapped) host memory, or
+// nullptr for pageable memory.
+void* mapped_view(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+// A whole small job (n <= kSmallUnits) on one device: the repair kernel runs
+// on the caller's pinned buffers through their mapped addresses, or — for
+// pageable buffers — on the device's small pinned buffer after one host
+// memcpy. Zero-copy PCIe traffic is fine at this size; what the call costs
+// is API latency, and this path has one launch and one synchronisation.
+u16m_status host_small(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out, int byte_order,
+                       unsigned long long* replacements) {
+  cudaError_t e = cudaSuccess;
+  if (!p->small) {
+    e = cudaHostAlloc(reinterpret_cast<void**>(&p->small), kSmallUnits * sizeof(uint16_t) + 64,
+                      cudaHostAllocMapped);
+    if (e == cudaSuccess)
+      e = cudaHostAlloc(reinterpret_cast<void**>(&p->small_count), sizeof(unsigned long long), cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      if (p->small) cudaFreeHost(p->small);
+      p->small = nullptr;
+      return cuda_fail(e, "small-job buffer");
+    }
+  }
+  const uint16_t* din = static_cast<const uint16_t*>(mapped_view(in));
+  uint16_t* dout = in == out ? const_cast<uint16_t*>(din) : static_cast<uint16_t*>(mapped_view(out));
+  const bool direct = din != nullptr && dout != nullptr;
+  if (!direct) {
+    std::memcpy(p->small, in, n * sizeof(uint16_t));
+    void* d = nullptr;
+    e = cudaHostGetDevicePointer(&d, p->small, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "small-job buffer mapping");
+    din = dout = static_cast<uint16_t*>(d);
+  }
+  const bool be = byte_order == U16M_BIG_ENDIAN;
+  if (byte_order < 0) {
+    e = u16m::launch_repair(din, n, dout, -1, -1, nullptr, nullptr, p->comp);
+  } else {
+    if (replacements) e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
+    if (e == cudaSuccess)
+      e = u16m::launch_fix_bytes(din, n, dout, be, replacements ? p->counter : nullptr, p->comp, -1, -1);
+    if (e == cudaSuccess && replacements)
+      e = cudaMemcpyAsync(p->small_count, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->comp);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "small-job repair");
+  e = cudaStreamSynchronize(p->comp);
+  if (e != cudaSuccess) return cuda_fail(e, "small-job sync");
+  if (!direct) std::memcpy(out, p->small, n * sizeof(uint16_t));
+  if (replacements) *replacements = *p->small_count;
+  return U16M_OK;
+}
+
 u16m_status host_device_job(int dev, const uint16_t* in, size_t n, uint16_t* out, size_t a, size_t b,
                             int byte_order, unsigned long long* replacements) {
   cudaError_t e = cudaSetDevice(dev);
@@ -414,6 +480,7 @@ u16m_status host_device_job(int dev, const uint16_t* in, size_t n, uint16_t* out
   HostPipe* p = pipe_for(dev, &st);
   if (p == nullptr) return st;
   std::lock_guard<std::mutex> lock(p->mu);  // one staged job per device at a time
+  if (a == 0 && b == n && n <= kSmallUnits) return host_small(p, in, n, out, byte_order, replacements);
   if (replacements) {
     e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
