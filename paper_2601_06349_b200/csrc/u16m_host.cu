@@ -58,6 +58,8 @@ struct HostPipe {
   cudaEvent_t staged[kStage] = {};
   uint16_t* small = nullptr;              // pinned + mapped, small jobs (kSmallUnits), lazily
   unsigned long long* small_count = nullptr;  // pinned, the small path's count read-back
+  unsigned long long* small_offs = nullptr;   // pinned, small scans' offsets read-back (kSmallOffs)
+  unsigned long long* small_dev = nullptr;    // device, small scans' offsets + count
   std::mutex mu;                          // one job per device pipeline at a time
 };
 
@@ -66,6 +68,7 @@ struct HostPipe {
 // device's address space), so a call is one launch + one synchronisation
 // instead of two DMAs, four events and three synchronisations.
 constexpr size_t kSmallUnits = size_t(64) << 10;
+constexpr size_t kSmallOffs = 4096;  // offsets read back with the count in one synchronisation
 
 // Streaming (non-temporal) copy for the staging copies: the destination is
 // written once and read next by a DMA engine or not at all, so bypassing the
@@ -430,20 +433,32 @@ void* mapped_view(const void* p) {
 // pageable buffers — on the device's small pinned buffer after one host
 // memcpy. Zero-copy PCIe traffic is fine at this size; what the call costs
 // is API latency, and this path has one launch and one synchronisation.
+// The small-job buffers of a device pipeline, allocated on first use.
+cudaError_t ensure_small(HostPipe* p) {
+  if (p->small) return cudaSuccess;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p->small), kSmallUnits * sizeof(uint16_t) + 64,
+                                cudaHostAllocMapped);
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(reinterpret_cast<void**>(&p->small_count), sizeof(unsigned long long), cudaHostAllocDefault);
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(reinterpret_cast<void**>(&p->small_offs), kSmallOffs * sizeof(unsigned long long),
+                      cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaMalloc(&p->small_dev, (kSmallUnits + 8) * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    if (p->small) cudaFreeHost(p->small);
+    if (p->small_count) cudaFreeHost(p->small_count);
+    if (p->small_offs) cudaFreeHost(p->small_offs);
+    p->small = nullptr;
+    p->small_count = p->small_offs = nullptr;
+    cudaGetLastError();
+  }
+  return e;
+}
+
 u16m_status host_small(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out, int byte_order,
                        unsigned long long* replacements) {
-  cudaError_t e = cudaSuccess;
-  if (!p->small) {
-    e = cudaHostAlloc(reinterpret_cast<void**>(&p->small), kSmallUnits * sizeof(uint16_t) + 64,
-                      cudaHostAllocMapped);
-    if (e == cudaSuccess)
-      e = cudaHostAlloc(reinterpret_cast<void**>(&p->small_count), sizeof(unsigned long long), cudaHostAllocDefault);
-    if (e != cudaSuccess) {
-      if (p->small) cudaFreeHost(p->small);
-      p->small = nullptr;
-      return cuda_fail(e, "small-job buffer");
-    }
-  }
+  cudaError_t e = ensure_small(p);
+  if (e != cudaSuccess) return cuda_fail(e, "small-job buffers");
   const uint16_t* din = static_cast<const uint16_t*>(mapped_view(in));
   uint16_t* dout = in == out ? const_cast<uint16_t*>(din) : static_cast<uint16_t*>(mapped_view(out));
   const bool direct = din != nullptr && dout != nullptr;
@@ -669,6 +684,43 @@ u16m_status unpaired_offsets_host(const uint16_t* in, size_t n, int byte_order, 
   HostPipe* p = pipe_for(dev, &st);
   if (p == nullptr) return st;
   std::lock_guard<std::mutex> lock(p->mu);
+  if (n <= kSmallUnits) {
+    // Small buffer: the scan kernels read host memory directly (mapped pinned
+    // memory: the caller's, or the small buffer after one memcpy — also for
+    // big-endian bytes, swapped there on the device); count and offsets come
+    // back with one synchronisation when limit <= kSmallOffs.
+    e = ensure_small(p);
+    if (e != cudaSuccess) return cuda_fail(e, "small-job buffers");
+    const bool be_small = byte_order == U16M_BIG_ENDIAN;
+    const uint16_t* din = be_small ? nullptr : static_cast<const uint16_t*>(mapped_view(in));
+    if (din == nullptr) {
+      std::memcpy(p->small, in, n * sizeof(uint16_t));
+      void* d = nullptr;
+      e = cudaHostGetDevicePointer(&d, p->small, 0);
+      if (e == cudaSuccess && be_small) e = u16m::launch_byteswap(static_cast<uint16_t*>(d), n, p->comp);
+      if (e != cudaSuccess) return cuda_fail(e, "small scan staging");
+      din = static_cast<const uint16_t*>(d);
+    }
+    unsigned long long* d_off = p->small_dev;
+    unsigned long long* d_cnt = p->small_dev + kSmallUnits;
+    e = u16m::launch_unpaired_offsets(din, n, limit, d_off, d_cnt, p->comp, -1, -1);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->small_count, d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->comp);
+    const bool one_sync = limit <= kSmallOffs;
+    if (e == cudaSuccess && one_sync)
+      e = cudaMemcpyAsync(p->small_offs, d_off, limit * sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->comp);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
+    if (e != cudaSuccess) return cuda_fail(e, "small scan");
+    const size_t cnt = static_cast<size_t>(*p->small_count);
+    if (one_sync) {
+      std::memcpy(offsets_out, p->small_offs, cnt * sizeof(unsigned long long));
+    } else if (cnt) {
+      e = cudaMemcpy(offsets_out, d_off, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_fail(e, "small scan offsets");
+    }
+    *count_out = cnt;
+    return U16M_OK;
+  }
   // Chunked, read-only scan: chunk c+1 moves H2D (straight from pinned memory,
   // or through a pinned bounce buffer filled by the CopyPool) while chunk c
   // is scanned with its neighbours' units as halos; the scan stops at the
