@@ -341,11 +341,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("U16M_BENCH_SHARE_GPU") == "1":
+        # code-path check of the N>1 line on a box with fewer GPUs than ranks
+        # (ranks share devices; the numbers are then meaningless)
+        local %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     distributed = world > 1 or args.force_dist
     if distributed:
-        pdist.init_process_group_for_repair("nccl", device_id=dev)
+        if os.environ.get("U16M_BENCH_SHARE_GPU") == "1":
+            pdist.init_process_group_for_repair("gloo")  # NCCL refuses two ranks on one GPU
+        else:
+            pdist.init_process_group_for_repair("nccl", device_id=dev)
     L = _lib.raw()
     cfg, per_gpu, modes, seed, desc = CONFIGS[args.config]
     if args.units:
