@@ -74,3 +74,27 @@ def test_reference_arm_under_torchrun_env():
                         "--steps", "2", "--warmup", "3", "--config", "c0"], capture_output=True, text=True,
                        timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+@pytest.mark.gpu
+def test_gpu_arm_multi_rank_line(cuda):
+    """The N>1 line through torchrun (two ranks; on a one-GPU box they share
+    it via U16M_BENCH_SHARE_GPU and a gloo group): IPC peer halos, summed
+    e2e, max-over-ranks timing, one JSON line from rank 0 — the code path the
+    driver's scaling run takes."""
+    import torch
+
+    env = dict(os.environ)
+    if torch.cuda.device_count() < 2:
+        env["U16M_BENCH_SHARE_GPU"] = "1"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+           "--warmup", "3", "--config", "c1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "shard2" and d["value"] > 0
+    assert d["run"]["halo"] == "ipc-peer-loads" and d["modes"]["inplace"]["output_check_well_formed"] is True
+    assert d["e2e"]["value"] > 0 and d["e2e"]["matches_device_result"] is True
