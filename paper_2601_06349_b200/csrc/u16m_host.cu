@@ -311,30 +311,14 @@ cudaError_t d2h_staged(HostPipe* p, void* dst, const void* src, size_t bytes) {
 // (36.7-40.8), chunks of 4-64 MiB (34-40 in place; ~20 us fixed cost per
 // chunk), a geometric ramp of the end chunks (no change).
 
-// One host job's share on one device: units [a, b) of the caller's buffers
-// (`in`/`out` hold n units), halo units read from the caller's input at
-// a-1 and b (-1 at the buffer's ends). The calling thread must have made
-// p->device current and hold p->mu. Device replacement counts (codec jobs)
-// accumulate in p->counter, which the caller reset.
-u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out, size_t a, size_t b,
-                       int byte_order, bool count) {
+// The staged copy-engine pipeline over a list of unit ranges of the caller's
+// buffers: per chunk H2D -> compute(dbuf, c0, len) on p->comp -> D2H. The
+// chunks may have any lengths up to pipe_chunk_units(). The calling thread
+// must have made p->device current and hold p->mu.
+template <class Compute>
+u16m_status pipeline_chunks(HostPipe* p, const uint16_t* in, uint16_t* out,
+                            const std::vector<std::pair<size_t, size_t>>& chunks, Compute compute) {
   cudaError_t e = cudaSuccess;
-  const bool be = byte_order == U16M_BIG_ENDIAN;
-  auto unit = [&](size_t i) -> int32_t {  // unit value of in[i] in the job's byte order
-    const uint32_t w = in[i];
-    return static_cast<int32_t>(be ? (((w & 0xFFu) << 8) | (w >> 8)) : w);
-  };
-  auto repair = [&](uint16_t* d, size_t c0, size_t len) {
-    // Halo units come from the caller's input at enqueue time. In place, a
-    // neighbouring chunk (or another device's range) may already have been
-    // written back; a rewritten neighbour is benign (a unit is only rewritten
-    // when no neighbour pairs with it, SURVEY.md §0 fact 3).
-    const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
-    const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
-    return byte_order < 0 ? u16m::launch_repair(d, len, d, left, right, nullptr, nullptr, p->comp)
-                          : u16m::launch_fix_bytes(d, len, d, be, count ? p->counter : nullptr, p->comp, left, right);
-  };
-  const size_t chunk = pipe_chunk_units();
   // Pageable host memory: the copy engines cannot DMA it directly, so every
   // chunk is copied (by the CopyPool threads) into a pinned bounce buffer,
   // moved H2D, repaired, moved D2H back into the same bounce buffer and
@@ -343,13 +327,12 @@ u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out,
   // single-threaded staging of pageable copies (7 GB/s on a 512 MiB job).
   if (!is_pinned(in) || !is_pinned(out)) {
     CopyPool& pool = CopyPool::get();
-    const size_t nchunks = (b - a + chunk - 1) / chunk;
+    const size_t nchunks = chunks.size();
     auto copy_out = [&](size_t c) -> cudaError_t {
       const int k = static_cast<int>(c % kStage);
       const cudaError_t r = cudaEventSynchronize(p->staged[k]);
       if (r != cudaSuccess) return r;
-      const size_t c0 = a + c * chunk, len = std::min(chunk, b - c0);
-      pool.copy(out + c0, p->stage[k], len * sizeof(uint16_t));
+      pool.copy(out + chunks[c].first, p->stage[k], chunks[c].second * sizeof(uint16_t));
       return cudaSuccess;
     };
     for (size_t c = 0; c < nchunks; c++) {
@@ -361,13 +344,13 @@ u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out,
       e = ensure_stage(p, k);
       if (e == cudaSuccess) e = ensure_dbuf(p, k);
       if (e != cudaSuccess) return cuda_fail(e, "staging buffers");
-      const size_t c0 = a + c * chunk, len = std::min(chunk, b - c0);
+      const size_t c0 = chunks[c].first, len = chunks[c].second;
       pool.copy(p->stage[k], in + c0, len * sizeof(uint16_t));
       e = cudaMemcpyAsync(p->dbuf[k], p->stage[k], len * 2, cudaMemcpyHostToDevice, p->h2d);
       if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
       cudaEventRecord(p->loaded[k], p->h2d);
       cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-      e = repair(p->dbuf[k], c0, len);
+      e = compute(p->dbuf[k], c0, len);
       if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
       cudaEventRecord(p->repaired[k], p->comp);
       cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
@@ -386,9 +369,8 @@ u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out,
   // Pinned: every chunk is DMA'd straight between the caller's buffer and a
   // device ring slot; chunk c's H2D waits only for the D2H that last used its
   // slot, so both copy engines stay busy while the kernel runs between them.
-  size_t c = 0;
-  for (size_t c0 = a; c0 < b; c0 += chunk, c++) {
-    const size_t len = std::min(chunk, b - c0);
+  for (size_t c = 0; c < chunks.size(); c++) {
+    const size_t c0 = chunks[c].first, len = chunks[c].second;
     const int k = static_cast<int>(c % kRing);
     if (c >= static_cast<size_t>(kRing)) {
       e = cudaStreamWaitEvent(p->h2d, p->drained[k], 0);
@@ -400,7 +382,7 @@ u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out,
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
     cudaEventRecord(p->loaded[k], p->h2d);
     cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
-    e = repair(p->dbuf[k], c0, len);
+    e = compute(p->dbuf[k], c0, len);
     if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
     cudaEventRecord(p->repaired[k], p->comp);
     cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
@@ -415,8 +397,35 @@ u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out,
   return U16M_OK;
 }
 
-// One device's whole share of a host job: select the device on this thread,
-// take its pipeline, reset its counter, run the range, read the count back.
+// One host job's share on one device: units [a, b) of the caller's buffers
+// (`in`/`out` hold n units), halo units read from the caller's input at
+// a-1 and b (-1 at the buffer's ends), in fixed-size chunks. Device
+// replacement counts (codec jobs) accumulate in p->counter, which the caller
+// reset.
+u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out, size_t a, size_t b,
+                       int byte_order, bool count) {
+  const bool be = byte_order == U16M_BIG_ENDIAN;
+  auto unit = [&](size_t i) -> int32_t {  // unit value of in[i] in the job's byte order
+    const uint32_t w = in[i];
+    return static_cast<int32_t>(be ? (((w & 0xFFu) << 8) | (w >> 8)) : w);
+  };
+  auto repair = [&](uint16_t* d, size_t c0, size_t len) {
+    // Halo units come from the caller's input at enqueue time. In place, a
+    // neighbouring chunk (or another device's range) may already have been
+    // written back; a rewritten neighbour is benign (a unit is only rewritten
+    // when no neighbour pairs with it, SURVEY.md §0 fact 3).
+    const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
+    const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
+    return byte_order < 0 ? u16m::launch_repair(d, len, d, left, right, nullptr, nullptr, p->comp)
+                          : u16m::launch_fix_bytes(d, len, d, be, count ? p->counter : nullptr, p->comp, left, right);
+  };
+  const size_t chunk = pipe_chunk_units();
+  std::vector<std::pair<size_t, size_t>> chunks;
+  chunks.reserve((b - a + chunk - 1) / chunk);
+  for (size_t c0 = a; c0 < b; c0 += chunk) chunks.emplace_back(c0, std::min(chunk, b - c0));
+  return pipeline_chunks(p, in, out, chunks, repair);
+}
+
 // Device-accessible address of pinned (page-locked, mapped) host memory, or
 // nullptr for pageable memory.
 void* mapped_view(const void* p) {
@@ -638,6 +647,65 @@ u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units,
   if (p == nullptr) return st;
   std::lock_guard<std::mutex> lock(p->mu);
   u16m::keep_pool_memory();
+  {
+    // Pipelined: chunks that end on string boundaries stream through the
+    // copy-engine pipeline like a plain host job (strings never straddle a
+    // chunk, so no halos), each repaired by the batched kernel addressed with
+    // the absolute offsets (one H2D of the whole offsets array first). Units
+    // before offsets[0] and after offsets[S] belong to no string: copied on
+    // the host. A string longer than a chunk takes the whole-buffer path below.
+    const size_t chunk = pipe_chunk_units();
+    const size_t A = static_cast<size_t>(offsets[0]), B = static_cast<size_t>(offsets[num_strings]);
+    std::vector<std::pair<size_t, size_t>> chunks;
+    std::vector<std::pair<size_t, size_t>> strs;  // [first string, end string) per chunk
+    bool fits = true;
+    for (size_t cur = A, sa = 0; cur < B;) {
+      size_t sb;
+      if (B - cur <= chunk) {
+        sb = num_strings;
+      } else {
+        // last string boundary in (cur, cur + chunk]
+        const int64_t* lim = std::upper_bound(offsets + sa, offsets + num_strings + 1, static_cast<int64_t>(cur + chunk));
+        sb = static_cast<size_t>(lim - offsets) - 1;
+        if (static_cast<size_t>(offsets[sb]) <= cur) {
+          fits = false;  // one string is longer than a chunk
+          break;
+        }
+      }
+      const size_t end = static_cast<size_t>(offsets[sb]);
+      chunks.emplace_back(cur, end - cur);
+      strs.emplace_back(sa, sb);
+      cur = end;
+      sa = sb;
+    }
+    if (fits) {
+      int64_t* d_off = nullptr;
+      const size_t off_bytes = (num_strings + 1) * sizeof(int64_t);
+      e = cudaMallocAsync(reinterpret_cast<void**>(&d_off), off_bytes, p->comp);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
+      if (e != cudaSuccess) return cuda_fail(e, "device offsets");
+      e = h2d_staged(p, d_off, offsets, off_bytes);
+      if (e != cudaSuccess) {
+        cudaFreeAsync(d_off, p->comp);
+        return cuda_fail(e, "offsets H2D");
+      }
+      size_t ci = 0;
+      auto repair = [&](uint16_t* d, size_t c0, size_t len) {
+        const auto [sa, sb] = strs[ci++];
+        // d holds units [c0, c0 + len): address it so that unit u is at d - c0 + u
+        return u16m::launch_batched_tiles(d - c0, c0 + len, d_off + sa, sb - sa, d - c0, p->comp, len);
+      };
+      st = pipeline_chunks(p, in, out, chunks, repair);
+      cudaFreeAsync(d_off, p->comp);
+      cudaStreamSynchronize(p->comp);
+      if (st != U16M_OK) return st;
+      if (out != in) {
+        if (A) CopyPool::get().copy(out, in, A * sizeof(uint16_t));
+        if (B < n_units) CopyPool::get().copy(out + B, in + B, (n_units - B) * sizeof(uint16_t));
+      }
+      return U16M_OK;
+    }
+  }
   const size_t data_bytes = n_units * sizeof(uint16_t), off_bytes = (num_strings + 1) * sizeof(int64_t);
   const size_t off_at = (data_bytes + 15) / 16 * 16;
   void* ws = nullptr;

@@ -56,8 +56,11 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
 // Batched form with the buffer length known: tile table pre-pass + one tile
 // per CTA (u16m_stream.cu). offsets[S] <= n_units.
 bool batched_tiles_enabled();
+// grid_units: size the grid and the tile table for this many units instead
+// of n_units (a job whose strings lie in a window of a larger coordinate
+// range, e.g. one chunk of the host pipeline addressed with absolute offsets).
 cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64_t* offsets, size_t num_strings,
-                                 uint16_t* out, cudaStream_t stream);
+                                 uint16_t* out, cudaStream_t stream, size_t grid_units = 0);
 
 
 // §8(f-3): byte-order-aware repair + replacement count (same 16-byte phase).

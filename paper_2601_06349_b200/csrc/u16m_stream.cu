@@ -656,7 +656,7 @@ static bool batched_pdl() {  // U16M_BATCHED_PDL=0: plain stream order (A/B)
 }
 
 cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64_t* offsets, size_t num_strings,
-                                 uint16_t* out, cudaStream_t stream) {
+                                 uint16_t* out, cudaStream_t stream, size_t grid_units) {
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
   const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
   const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
@@ -671,7 +671,7 @@ cudaError_t launch_batched_tiles(const uint16_t* in, size_t n_units, const int64
   s.prefetch_tiles = 0;
   constexpr uint64_t kTileUnits = kSCtaVecs * 8;
   const uint64_t count = static_cast<uint64_t>(num_strings) + 1;
-  const uint64_t ntiles_max = (static_cast<uint64_t>(n_units) + 16) / kTileUnits + 2;
+  const uint64_t ntiles_max = (static_cast<uint64_t>(grid_units ? grid_units : n_units) + 16) / kTileUnits + 2;
   const uint64_t nwtiles_max = ntiles_max * (kSThreads / 32);  // even
   uint64_t* table = nullptr;  // first string starting in or after each warp tile
   keep_pool_memory();

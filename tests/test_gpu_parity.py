@@ -809,3 +809,20 @@ def test_concurrent_callers_on_their_own_streams(P, cuda):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("chunk_kib", ["64", "1024", ""])
+def test_batched_host_pipeline_chunks(cuda, chunk_kib):
+    """The pipelined batched host path: chunks end on string boundaries (no
+    halos), head / tail outside the strings copied on the host, and a string
+    longer than a chunk falls back to the whole-buffer path — exact for every
+    chunk size."""
+    import subprocess
+    import sys
+
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gpu_helpers", "batched_host_check.py")
+    env = {k: v for k, v in os.environ.items() if not k.startswith("U16M_")}
+    if chunk_kib:
+        env["U16M_PIPE_CHUNK_KIB"] = chunk_kib
+    r = subprocess.run([sys.executable, helper], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
