@@ -17,3 +17,7 @@ for c in c4copy c4i c3; do
 done
 timeout 900 ncu --set full --clock-control none -k regex:stream_kernel -s 1 -c 1 -o $O/prof_count_c4 python scripts/count_probe.py > $O/ncu_count.log 2>&1
 echo "ncu count rc=$?" >> $O/ncu_rc.txt
+# keep gpurun_out small (the merge-back limit is 64 MiB): text summaries only
+for r in $O/prof_*.ncu-rep; do python scripts/ncu_summary.py $r > ${r%.ncu-rep}.txt 2>&1; done
+python scripts/launch_summary.py $O/launches_default_cmd.csv > $O/launches_default_cmd_summary.txt 2>&1
+rm -f $O/prof_*.ncu-rep
