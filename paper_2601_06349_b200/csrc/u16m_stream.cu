@@ -474,10 +474,22 @@ __device__ __forceinline__ void scan_window(int64_t p, int64_t A0, int64_t A1, i
 // kShift > 0 (copy only): `out` has a different 16-byte phase than `in`;
 // s.out is out's 16-byte-aligned base, s.out_units the caller's out pointer,
 // and vectors are stored shifted as in stream_shift_kernel (q: vector offset).
+// The tile table is written by tile_first_kernel WHILE this grid is already
+// running (programmatic dependent launch), so it must not be read through the
+// read-only path: with `const __restrict__` the compiler emits
+// LDG.CONSTANT and may hoist it above griddepcontrol.wait (a build that did
+// read stale entries). It is read with ld.global.cg in inline asm that is
+// ordered after the wait.
+__device__ __forceinline__ uint64_t ld_table(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <bool kInPlace, int kGran, int kShift = 0>
 __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, const int64_t* __restrict__ offsets,
                                                                     uint64_t count, uint32_t phase,
-                                                                    const uint64_t* __restrict__ tile_first,
+                                                                    const uint64_t* tile_first,
                                                                     uint64_t nwt, int64_t n_units, int64_t q) {
   static_assert(kShift == 0 || !kInPlace, "in place is always the same phase");
   const int lane = threadIdx.x & 31;
@@ -528,8 +540,8 @@ __global__ void __launch_bounds__(kSThreads, 4) batched_tile_kernel(Span s, cons
   // instead, which only finds whether one starts exactly at A1.
   const uint64_t wt = (wv0 - vbeg) / kSWarpVecs;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the tile table is complete and visible
-  const uint64_t c0 = tile_first[wt];
-  const uint64_t c1 = wt + 1 < nwt ? tile_first[wt + 1] : kNoStart;
+  const uint64_t c0 = ld_table(tile_first + wt);
+  const uint64_t c1 = wt + 1 < nwt ? ld_table(tile_first + wt + 1) : kNoStart;
   const uint64_t first = c0 != kNoStart ? c0 : (c1 < count ? c1 : count);
   StartScan st{0, false};
   for (uint64_t scan = first;;) {
