@@ -78,6 +78,8 @@ _L.u16m_to_well_formed_host_multi.restype = _st
 _L.u16m_fix_utf16_bytes_host_multi.argtypes = [_vp, _sz, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong),
                                                ctypes.c_int, _vp]
 _L.u16m_fix_utf16_bytes_host_multi.restype = _st
+_L.u16m_unpaired_offsets_bytes_host.argtypes = [_vp, _sz, ctypes.c_int, _sz, _vp, ctypes.POINTER(ctypes.c_size_t)]
+_L.u16m_unpaired_offsets_bytes_host.restype = _st
 
 
 class U16MError(RuntimeError):

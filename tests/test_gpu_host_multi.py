@@ -161,3 +161,42 @@ def test_codec_host_multi_ranges(P, cuda, big):
     h = buf.view(">u2").astype(np.uint16) if big else buf
     assert np.array_equal(h, e) and cnt.value == int((x != e).sum())
     assert L.u16m_fix_utf16_bytes_host_multi(hin.data_ptr(), n, hout.data_ptr(), 2, None, 1, _ids(0)) == 1
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_small_host_jobs_zero_copy(P, cuda, pinned):
+    """Host jobs of at most 64 Ki units run the kernel on mapped pinned memory
+    (the caller's, or the small staging buffer): plain repair copy / in place
+    at odd phases, the byte-order-fused form with its count, and the
+    validation scan (LE and BE) — all equal to the oracle."""
+    L = P._lib.raw()
+    rng = np.random.default_rng(17)
+    for n in (1, 7, 8, 9, 4095, 65535, 65536):
+        x = rng.integers(0, 65536, n).astype(np.uint16)
+        x[rng.integers(0, n, max(1, n // 50))] = 0xD800
+        e = O.stencil(x)
+        for phase in (0, 1, 3):
+            base = torch.zeros(n + 16, dtype=torch.int16)
+            obase = torch.zeros(n + 16, dtype=torch.int16)
+            if pinned:
+                base, obase = base.pin_memory(), obase.pin_memory()
+            src = base[phase:phase + n]
+            src.copy_(torch.from_numpy(x.view(np.int16)))
+            out = obase[(phase + 2) % 8:(phase + 2) % 8 + n]
+            assert L.u16m_to_well_formed_host(src.data_ptr(), n, out.data_ptr()) == 0
+            assert (out.numpy().view(np.uint16) == e).all(), (n, phase, "copy")
+            for be in (False, True):
+                raw = (x.astype(">u2") if be else x).view(np.uint16)
+                src.copy_(torch.from_numpy(raw.view(np.int16).copy()))
+                cnt = ctypes.c_ulonglong(0)
+                assert L.u16m_fix_utf16_bytes_host(src.data_ptr(), n, src.data_ptr(), int(be), ctypes.byref(cnt)) == 0
+                got = src.numpy().view(np.uint16)
+                got = got.view(">u2").astype(np.uint16) if be else got
+                assert (got == e).all() and cnt.value == int((x != e).sum()), (n, phase, be)
+                src.copy_(torch.from_numpy(raw.view(np.int16).copy()))
+                offs = (ctypes.c_ulonglong * 16)()
+                found = ctypes.c_size_t(0)
+                assert L.u16m_unpaired_offsets_bytes_host(src.data_ptr(), n, int(be), 16, offs,
+                                                          ctypes.byref(found)) == 0
+                exp = np.flatnonzero(x != e)[:16]
+                assert found.value == exp.size and list(offs[:found.value]) == exp.tolist(), (n, phase, be)
