@@ -647,85 +647,67 @@ u16m_status u16m_to_well_formed_batched_host(const uint16_t* in, size_t n_units,
   if (p == nullptr) return st;
   std::lock_guard<std::mutex> lock(p->mu);
   u16m::keep_pool_memory();
-  {
-    // Pipelined: chunks that end on string boundaries stream through the
-    // copy-engine pipeline like a plain host job (strings never straddle a
-    // chunk, so no halos), each repaired by the batched kernel addressed with
-    // the absolute offsets (one H2D of the whole offsets array first). Units
-    // before offsets[0] and after offsets[S] belong to no string: copied on
-    // the host. A string longer than a chunk takes the whole-buffer path below.
-    const size_t chunk = pipe_chunk_units();
-    const size_t A = static_cast<size_t>(offsets[0]), B = static_cast<size_t>(offsets[num_strings]);
-    std::vector<std::pair<size_t, size_t>> chunks;
-    std::vector<std::pair<size_t, size_t>> strs;  // [first string, end string) per chunk
-    bool fits = true;
-    for (size_t cur = A, sa = 0; cur < B;) {
-      size_t sb;
-      if (B - cur <= chunk) {
-        sb = num_strings;
-      } else {
-        // last string boundary in (cur, cur + chunk]
-        const int64_t* lim = std::upper_bound(offsets + sa, offsets + num_strings + 1, static_cast<int64_t>(cur + chunk));
-        sb = static_cast<size_t>(lim - offsets) - 1;
-        if (static_cast<size_t>(offsets[sb]) <= cur) {
-          fits = false;  // one string is longer than a chunk
-          break;
-        }
-      }
-      const size_t end = static_cast<size_t>(offsets[sb]);
-      chunks.emplace_back(cur, end - cur);
-      strs.emplace_back(sa, sb);
-      cur = end;
-      sa = sb;
-    }
-    if (fits) {
-      int64_t* d_off = nullptr;
-      const size_t off_bytes = (num_strings + 1) * sizeof(int64_t);
-      e = cudaMallocAsync(reinterpret_cast<void**>(&d_off), off_bytes, p->comp);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
-      if (e != cudaSuccess) return cuda_fail(e, "device offsets");
-      e = h2d_staged(p, d_off, offsets, off_bytes);
-      if (e != cudaSuccess) {
-        cudaFreeAsync(d_off, p->comp);
-        return cuda_fail(e, "offsets H2D");
-      }
-      size_t ci = 0;
-      auto repair = [&](uint16_t* d, size_t c0, size_t len) {
-        const auto [sa, sb] = strs[ci++];
-        // d holds units [c0, c0 + len): address it so that unit u is at d - c0 + u
-        return u16m::launch_batched_tiles(d - c0, c0 + len, d_off + sa, sb - sa, d - c0, p->comp, len);
-      };
-      st = pipeline_chunks(p, in, out, chunks, repair);
-      cudaFreeAsync(d_off, p->comp);
-      cudaStreamSynchronize(p->comp);
-      if (st != U16M_OK) return st;
-      if (out != in) {
-        if (A) CopyPool::get().copy(out, in, A * sizeof(uint16_t));
-        if (B < n_units) CopyPool::get().copy(out + B, in + B, (n_units - B) * sizeof(uint16_t));
-      }
-      return U16M_OK;
-    }
-  }
-  const size_t data_bytes = n_units * sizeof(uint16_t), off_bytes = (num_strings + 1) * sizeof(int64_t);
-  const size_t off_at = (data_bytes + 15) / 16 * 16;
-  void* ws = nullptr;
-  e = cudaMallocAsync(&ws, off_at + off_bytes, p->comp);
+  // The buffer streams through the copy-engine pipeline in fixed chunks, like
+  // a plain host job; the offsets array goes H2D once. Per chunk [c0, c1):
+  // the strings lying wholly inside run the batched tile kernel (addressed
+  // with the absolute offsets), and a string cut by the chunk's start and/or
+  // end is repaired on its in-chunk segment by the plain kernel with the real
+  // neighbour unit (read from the caller's input) as the halo on the cut side
+  // and "outside" on the string's own end — so strings of any length, even
+  // longer than a chunk, and buffers larger than device memory stream
+  // through. Units in no string pass through unchanged.
+  const size_t S = num_strings;
+  const size_t off_bytes = (S + 1) * sizeof(int64_t);
+  int64_t* d_off = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void**>(&d_off), off_bytes, p->comp);
   if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
-  if (e != cudaSuccess) return cuda_fail(e, "device buffer");
-  auto* d_data = static_cast<uint16_t*>(ws);
-  auto* d_off = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + off_at);
-  e = h2d_staged(p, d_data, in, data_bytes);
-  if (e == cudaSuccess) e = h2d_staged(p, d_off, offsets, off_bytes);
-  if (e == cudaSuccess) {
-    const cudaError_t k = u16m::launch_batched_tiles(d_data, n_units, d_off, num_strings, d_data, p->comp);
-    e = k != cudaSuccess ? k : cudaStreamSynchronize(p->comp);
+  if (e != cudaSuccess) return cuda_fail(e, "device offsets");
+  e = h2d_staged(p, d_off, offsets, off_bytes);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(d_off, p->comp);
+    return cuda_fail(e, "offsets H2D");
   }
-  if (e == cudaSuccess) e = d2h_staged(p, out, d_data, data_bytes);
-  cudaFreeAsync(ws, p->comp);
-  const cudaError_t f = cudaStreamSynchronize(p->comp);
-  if (e != cudaSuccess) return cuda_fail(e, "batched host repair");
-  if (f != cudaSuccess) return cuda_fail(f, "batched host repair");
-  return U16M_OK;
+  const int64_t* o_end = offsets + S + 1;
+  auto repair = [&](uint16_t* d, size_t c0, size_t len) -> cudaError_t {
+    const size_t c1 = c0 + len;
+    const int64_t a = static_cast<int64_t>(c0), b = static_cast<int64_t>(c1);
+    // lo: first boundary >= c0; hi: first boundary > c1
+    const size_t lo = static_cast<size_t>(std::lower_bound(offsets, o_end, a) - offsets);
+    const size_t hi = static_cast<size_t>(std::upper_bound(offsets, o_end, b) - offsets);
+    auto plain = [&](size_t u0, size_t u1, int32_t left, int32_t right) -> cudaError_t {
+      if (u1 <= u0) return cudaSuccess;
+      uint16_t* q = d + (u0 - c0);
+      return u16m::launch_repair(q, u1 - u0, q, left, right, nullptr, nullptr, p->comp);
+    };
+    cudaError_t r = cudaSuccess;
+    // a string that started before c0 and is still running at c0
+    const bool head_cut = lo >= 1 && lo <= S && offsets[lo] > a;
+    if (head_cut) {
+      const size_t e0 = static_cast<size_t>(offsets[lo]);
+      if (e0 > c1)  // the whole chunk is inside one string
+        return plain(c0, c1, in[c0 - 1], in[c1]);
+      r = plain(c0, e0, in[c0 - 1], -1);
+      if (r != cudaSuccess) return r;
+    }
+    // strings wholly inside: [lo, hi - 1)
+    if (hi >= 1 && hi - 1 > lo) {
+      const size_t sa = lo, sb = hi - 1;
+      r = u16m::launch_batched_tiles(d - c0, c1, d_off + sa, sb - sa, d - c0, p->comp, len);
+      if (r != cudaSuccess) return r;
+    }
+    // a string that starts inside the chunk and runs past c1
+    if (hi >= 1 && hi <= S && offsets[hi - 1] < b && offsets[hi - 1] >= a)
+      r = plain(static_cast<size_t>(offsets[hi - 1]), c1, -1, in[c1]);
+    return r;
+  };
+  const size_t chunk = pipe_chunk_units();
+  std::vector<std::pair<size_t, size_t>> chunks;
+  chunks.reserve((n_units + chunk - 1) / chunk);
+  for (size_t c0 = 0; c0 < n_units; c0 += chunk) chunks.emplace_back(c0, std::min(chunk, n_units - c0));
+  st = pipeline_chunks(p, in, out, chunks, repair);
+  cudaFreeAsync(d_off, p->comp);
+  cudaStreamSynchronize(p->comp);
+  return st;
 }
 
 }  // extern "C"

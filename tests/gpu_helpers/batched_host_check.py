@@ -41,12 +41,16 @@ def main():
     # many short strings (and runs of empty ones), head and tail outside every string
     cuts = np.sort(np.concatenate([rng.integers(3, n - 5, 40_000), np.full(50, 1_000_000)]))
     check(x, np.concatenate([[3], cuts, [n - 5]]).astype(np.int64), "short strings")
-    # one string longer than a chunk (the whole-buffer path)
+    # strings longer than a chunk (cut by chunk edges: plain-kernel segments with real halos)
     check(x, np.array([0, 10, n - 10, n], np.int64), "long string")
+    check(x, np.array([5, 5, n - 7], np.int64), "one long string, empty first")
+    # long and short strings mixed, and strings cut exactly one unit into a chunk
+    chunk = int(os.environ.get("U16M_PIPE_CHUNK_KIB", "32768")) * 512
+    mix = np.sort(np.concatenate([rng.integers(0, n, 300), [chunk + 1, 2 * chunk - 1, 2 * chunk + 1]]))
+    check(x, np.concatenate([[0], mix[mix < n], [n]]).astype(np.int64), "mixed lengths")
     # only empty strings
     check(x, np.full(1001, 12345, np.int64), "empty strings")
     # strings ending exactly on multiples of the chunk size
-    chunk = int(os.environ.get("U16M_PIPE_CHUNK_KIB", "32768")) * 512
     edges = np.arange(0, n, max(1, chunk // 4), dtype=np.int64)
     check(x, np.concatenate([edges, [n]]).astype(np.int64), "chunk-aligned strings")
     print("OK")
