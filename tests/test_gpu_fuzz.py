@@ -93,3 +93,17 @@ def test_fuzz_all_entry_points(P, cuda):
             bo.copy_(src)
             P.to_well_formed_batched(src, torch.from_numpy(offs).cuda(), out=bo)
             assert (host(bo) == eb).all(), ("batched phases", it, n, pi, po)
+
+
+def test_fuzz_batched_host_pipeline(cuda):
+    """Random batches through the pipelined batched host form with 8 KiB
+    chunks (4096 units), so strings are cut by many chunk edges."""
+    import os
+    import subprocess
+    import sys
+
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gpu_helpers", "batched_host_fuzz.py")
+    env = {k: v for k, v in os.environ.items() if not k.startswith("U16M_PIPE")}
+    env["U16M_PIPE_CHUNK_KIB"] = "8"
+    r = subprocess.run([sys.executable, helper], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
