@@ -56,7 +56,23 @@ u16m_status check_device_ptr(const void* p, const char* name) {
     cudaGetLastError();
     return fail(U16M_ERR_NOT_DEVICE_MEMORY, std::string(name) + " is not a CUDA-visible pointer");
   }
-  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return U16M_OK;
+  if (a.type == cudaMemoryTypeDevice) {
+    // Memory of another GPU than the current one is only usable over peer
+    // access; without it the kernel would fault (a sticky error that ends the
+    // CUDA context), so refuse it here with a readable message.
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && a.device != cur) {
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, cur, a.device) != cudaSuccess || !can) {
+        cudaGetLastError();
+        return fail(U16M_ERR_NOT_DEVICE_MEMORY, std::string(name) + " is memory of cuda:" + std::to_string(a.device) +
+                                                    ", the current device is cuda:" + std::to_string(cur) +
+                                                    " and has no peer access to it (cudaSetDevice first)");
+      }
+    }
+    return U16M_OK;
+  }
+  if (a.type == cudaMemoryTypeManaged) return U16M_OK;
   if (a.type == cudaMemoryTypeHost && a.devicePointer != nullptr) return U16M_OK;
   return fail(U16M_ERR_NOT_DEVICE_MEMORY,
               std::string(name) + " is host memory; use u16m_to_well_formed_host or the C++ API");
