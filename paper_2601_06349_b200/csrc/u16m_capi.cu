@@ -69,6 +69,10 @@ u16m_status check_device_ptr(const void* p, const char* name) {
                                                     ", the current device is cuda:" + std::to_string(cur) +
                                                     " and has no peer access to it (cudaSetDevice first)");
       }
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(a.device, 0);  // idempotent (NVLink peer loads)
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled)
+        return cuda_fail(pe, "enabling peer access");
+      cudaGetLastError();
     }
     return U16M_OK;
   }
