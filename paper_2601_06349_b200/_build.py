@@ -6,6 +6,11 @@ Every .cu in csrc/ is compiled with nvcc for `-gencode arch=compute_100a,
 code=sm_100a -lineinfo -O3` and linked (static cudart) into
 paper_2601_06349_b200/libu16m.so, next to this file, so the built library
 travels to the GPU box with the repo snapshot.
+
+libu16m.so holds the default kernel path only. The kernel families kept for
+A/B measurements (U16M_KERNEL=tma|ldg|general) are compiled only with
+-DU16M_AB_VARIANTS, into a second library libu16m_ab.so of the same ABI that
+tests/test_gpu_variants.py and the A/B scripts load through U16M_LIBRARY.
 """
 from __future__ import annotations
 
@@ -20,6 +25,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libu16m.so")
+LIB_AB = os.path.join(PKG, "libu16m_ab.so")   # + the A/B kernel families
+AB_SOURCES = ("u16m_kernels.cu", "u16m_tma.cu")  # the files that test U16M_AB_VARIANTS
 CLI = os.path.join(PKG, "u16m")
 CLI_SRC = os.path.join(PKG, "tools", "u16m_cli.cpp")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -39,9 +46,9 @@ def _deps() -> list[str]:
 
 
 def needs_build() -> bool:
-    if not os.path.exists(LIB) or not os.path.exists(CLI):
+    if not all(os.path.exists(p) for p in (LIB, LIB_AB, CLI)):
         return True
-    t = min(os.path.getmtime(LIB), os.path.getmtime(CLI))
+    t = min(os.path.getmtime(p) for p in (LIB, LIB_AB, CLI))
     return any(os.path.getmtime(p) > t for p in _deps() + [CLI_SRC])
 
 
@@ -56,9 +63,10 @@ def build_cli() -> str:
     return CLI
 
 
-def _compile(src: str) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    cmd = [NVCC, *FLAGS, "-Xptxas", "-v", "-c", src, "-o", obj]
+def _compile(job: tuple[str, bool]) -> str:
+    src, ab = job
+    obj = os.path.join(BUILD, os.path.basename(src) + (".ab.o" if ab else ".o"))
+    cmd = [NVCC, *FLAGS, *(["-DU16M_AB_VARIANTS"] if ab else []), "-Xptxas", "-v", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -71,14 +79,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
+    srcs = _sources()
+    jobs = [(s, False) for s in srcs] + [(s, True) for s in srcs if os.path.basename(s) in AB_SOURCES]
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(_compile, _sources()))
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+        objs = dict(zip(jobs, ex.map(_compile, jobs)))
+    for lib, ab in ((LIB, False), (LIB_AB, True)):
+        use = [objs[(s, ab and os.path.basename(s) in AB_SOURCES)] for s in srcs]
+        tmp = lib + ".tmp"
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *use, "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, lib)
     build_cli()
     if verbose:
         print("built", LIB, "and", CLI)

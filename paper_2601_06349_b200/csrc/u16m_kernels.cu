@@ -367,17 +367,20 @@ uint64_t tiles_for(const Span& s) {
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-// Kernel family selection. Default ("auto"): copy / in-place run the rolling
-// register-pipeline stream kernel (u16m_stream.cu; measured best: 6.9 TB/s
-// copy, config 1 in 131 us); the length-aware batched entry runs the batched
-// tile kernel (u16m_stream.cu) and the length-less one the TMA-pipelined
-// kernel (its producer warp walks the offsets off the consumers' critical
-// path; a persistent grid needs no length).
-// U16M_KERNEL overrides for A/B runs (profiles/README.md has the numbers):
-// "tma" (TMA-pipelined for everything), "ldg" (register-staged everywhere;
-// the length-less batched entry then uses the general kernel), "general"
-// (the 4-vector general kernel for everything).
+// Kernel family selection. Copy / in-place run the rolling register-pipeline
+// stream kernel (u16m_stream.cu; measured best: 6.9 TB/s copy, config 1 in
+// 131 us); the batched form runs the batched tile kernel (u16m_stream.cu)
+// whenever the buffer can be bounded, else the TMA-pipelined kernel (its
+// producer warp walks the offsets off the consumers' critical path; a
+// persistent grid needs no length).
+// The other families are A/B material only and are compiled in only with
+// -DU16M_AB_VARIANTS (libu16m_ab.so, `_build.py --ab`; the product library
+// holds the default path alone). There, U16M_KERNEL selects: "tma"
+// (TMA-pipelined for everything), "ldg" (register-staged everywhere; the
+// length-less batched entry then uses the general kernel), "general" (the
+// 4-vector general kernel for everything). profiles/README.md has the numbers.
 enum KernelChoice { kChoiceAuto = 0, kChoiceTma = 1, kChoiceGeneral = 2, kChoiceLdg = 3 };
+#ifdef U16M_AB_VARIANTS
 // (kChoiceGeneral and kChoiceAuto share the register-staged kernel for plain
 // streams; they differ for the batched form.)
 static int kernel_choice() {
@@ -395,6 +398,9 @@ template <int kGran>
 static cudaError_t launch_inplace(const Span& s, uint64_t grid, cudaStream_t stream) {
   return launch<kInPlace, true, false, kGran>(s, kNoBatch, kNoScan, grid, stream);
 }
+#else
+static constexpr int kernel_choice() { return kChoiceAuto; }
+#endif
 
 cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
                                const uint16_t* left_ptr, const uint16_t* right_ptr, int part,
@@ -402,6 +408,7 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
   if (n == 0) return cudaSuccess;
   bool same = false;
   Span s = make_span(in, n, out, left, right, left_ptr, right_ptr, &same);
+#ifdef U16M_AB_VARIANTS
   const uint64_t ntiles = tiles_for(s);
   const int choice = kernel_choice();
   if ((in == out || same) && choice == kChoiceTma && n >= kTmaMinUnits) {
@@ -409,15 +416,18 @@ cudaError_t launch_repair_part(const uint16_t* in, size_t n, uint16_t* out, int3
     if (part == kTilesInterior) return cudaSuccess;
     return launch_repair_tma(in, n, out, left, right, left_ptr, right_ptr, stream);
   }
-  if ((in == out || same) && (choice == kChoiceAuto || choice == kChoiceLdg)) return launch_stream(s, part, stream);
-  if (choice == kChoiceAuto || choice == kChoiceLdg) return launch_stream_shift(s, out, part, stream);
-  s.tile_sel = part;
-  const uint64_t grid = part == kTilesAll ? ntiles
-                        : part == kTilesEdges ? (ntiles < 2 ? ntiles : 2)
-                                              : (ntiles > 2 ? ntiles - 2 : 0);
-  if (in == out) return launch_inplace<kDefaultInplaceGran>(s, grid, stream);
-  if (same) return launch<kCopy, true, false>(s, kNoBatch, kNoScan, grid, stream);
-  return launch<kCopy, false, false>(s, kNoBatch, kNoScan, grid, stream);
+  if (choice == kChoiceGeneral) {
+    s.tile_sel = part;
+    const uint64_t grid = part == kTilesAll ? ntiles
+                          : part == kTilesEdges ? (ntiles < 2 ? ntiles : 2)
+                                                : (ntiles > 2 ? ntiles - 2 : 0);
+    if (in == out) return launch_inplace<kDefaultInplaceGran>(s, grid, stream);
+    if (same) return launch<kCopy, true, false>(s, kNoBatch, kNoScan, grid, stream);
+    return launch<kCopy, false, false>(s, kNoBatch, kNoScan, grid, stream);
+  }
+#endif
+  if (in == out || same) return launch_stream(s, part, stream);
+  return launch_stream_shift(s, out, part, stream);
 }
 
 cudaError_t launch_fix_bytes(const void* in, size_t n, void* out, bool big_endian, unsigned long long* count,
@@ -600,10 +610,12 @@ cudaError_t launch_batched(const uint16_t* in, const int64_t* offsets, size_t nu
   const BatchArgs b{offsets, static_cast<uint64_t>(num_strings) + 1, ph};
   // Persistent grid: the range is only known on the device.
   const uint64_t grid = static_cast<uint64_t>(sm_count_for_current_device()) * 8;
+#ifdef U16M_AB_VARIANTS
   const bool same = (ia & 15u) == (oa & 15u);
   if (in == out) return launch<kInPlace, true, true>(s, b, kNoScan, grid, stream);
   if (same) return launch<kCopy, true, true>(s, b, kNoScan, grid, stream);
-  return launch<kCopy, false, true>(s, b, kNoScan, grid, stream);
+#endif
+  return launch<kCopy, false, true>(s, b, kNoScan, grid, stream);  // out at another 16-byte phase
 }
 
 }  // namespace u16m

@@ -327,6 +327,7 @@ cudaError_t launch_tma(const Span& s, const BatchArgsT& b, uint64_t ntiles_hint,
 
 }  // namespace tma
 
+#ifdef U16M_AB_VARIANTS  // plain (non-batched) streams through the TMA ring: A/B only
 cudaError_t launch_repair_tma(const uint16_t* in, size_t n, uint16_t* out, int32_t left, int32_t right,
                               const uint16_t* left_ptr, const uint16_t* right_ptr, cudaStream_t stream) {
   const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
@@ -349,6 +350,7 @@ cudaError_t launch_repair_tma(const uint16_t* in, size_t n, uint16_t* out, int32
   if (in != out) return tma::launch_tma<0, false, 1>(s, b, ntiles, stream);
   return tma::launch_tma<1, false, kDefaultInplaceGran>(s, b, ntiles, stream);
 }
+#endif
 
 cudaError_t launch_batched_tma(const uint16_t* in, const int64_t* offsets, size_t num_strings, uint16_t* out,
                                cudaStream_t stream) {

@@ -35,6 +35,28 @@ def test_exports_every_declared_symbol(header):
         assert re.search(rf"\bT {n}\b", out), n
 
 
+def test_ab_library_same_abi_and_product_library_holds_default_path_only():
+    """libu16m_ab.so (-DU16M_AB_VARIANTS) exports the same ABI; the A/B-only
+    kernel instantiations (plain streams through the TMA ring, the general
+    kernel for plain copy / in place) are absent from the product library."""
+    ab = os.path.join(os.path.dirname(P.lib_path()), "libu16m_ab.so")
+    assert os.path.exists(ab)
+    def dyn(path):
+        out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+        return sorted(l.split()[-1] for l in out.splitlines() if " T " in l and "launch_repair_tma" not in l)
+    assert dyn(ab) == dyn(P.lib_path())
+    def kernels(path):
+        out = subprocess.run(["cuobjdump", "-elf", path], capture_output=True, text=True).stdout
+        return set(re.findall(r"\.text\.(_Z\S+)", out))
+    prod, full = kernels(P.lib_path()), kernels(ab)
+    assert prod < full
+    extra = "\n".join(sorted(full - prod))
+    assert "repair_tma_kernel" in extra and "repair_kernel" in extra
+    # what the product path launches is all there
+    for k in ("stream_kernel", "stream_shift_kernel", "batched_tile_kernel", "tile_first_kernel", "repair_tma_kernel"):
+        assert any(k in n for n in prod), k
+
+
 def test_cpp_api_symbols_exported():
     out = subprocess.run(["nm", "-DC", "--defined-only", P.lib_path()], capture_output=True, text=True).stdout
     for sym in ("utf16mend::to_well_formed(", "utf16mend::to_well_formed_in_place(",
