@@ -529,6 +529,62 @@ def test_config4_shards(P, cuda):
     assert P.count_unpaired(y) == 0
 
 
+@pytest.mark.slow
+def test_beyond_32bit_unit_indices(P, cuda):
+    """A job of more than 2^32 units (8.6 GB): every unit index past 2^32 needs
+    64-bit arithmetic in the kernels. Plain copy / in place / count / offsets
+    and the batched form over strings lying on both sides of 2^32; exact
+    against the oracle around 2^32 and over the tail, size-independent
+    properties over the whole buffer."""
+    free, _ = torch.cuda.mem_get_info()
+    n = (1 << 32) + (1 << 21) + 5
+    if free < 5 * 2 * n:
+        pytest.skip("needs ~45 GB of free device memory")
+    x = P._lib.gen_config(1, n, seed=33)                   # uniform units: rewrites everywhere
+    y = P.to_well_formed(x)
+
+    def window(a, b):
+        lo, hi = max(0, a - 1), min(n, b + 1)
+        e = O.stencil_mt(host(x[lo:hi]))
+        return e[a - lo:a - lo + (b - a)]
+    edge = (1 << 32) - (1 << 20)
+    assert (host(y[edge:n]) == window(edge, n)).all()      # across 2^32 and to the ragged end
+    assert (host(y[:1 << 20]) == window(0, 1 << 20)).all()
+    rewrites = sum(int((x[a:a + (1 << 28)] != y[a:a + (1 << 28)]).sum()) for a in range(0, n, 1 << 28))
+    assert P.count_unpaired(x) == rewrites
+    assert P.count_unpaired(y) == 0
+    # offsets: the last ones lie past 2^32
+    tail_pos = (x[edge:] != y[edge:]).nonzero().flatten() + edge
+    lim = rewrites - tail_pos.numel() + 1000
+    offs = P.unpaired_offsets_device(x, limit=lim)
+    assert offs.numel() == lim
+    assert torch.equal(offs[-1000:], tail_pos[:1000])
+    assert int(offs[-1]) > (1 << 32) - (1 << 20)
+    del offs
+    z = x.clone()
+    P.to_well_formed_(z)
+    for a in range(0, n, 1 << 28):
+        assert torch.equal(z[a:a + (1 << 28)], y[a:a + (1 << 28)]), a   # in place == copy
+    del z
+    # batched: one long string up to just below 2^32, short strings across it, a long tail string
+    cut = (1 << 32) - 3000
+    lens = np.random.default_rng(5).integers(0, 700, 20)
+    mids = cut + np.concatenate([[0], np.cumsum(lens)])
+    offsets = np.concatenate([[7], mids, [n - 11]]).astype(np.int64)
+    o = torch.from_numpy(offsets).cuda()
+    w = torch.full_like(x, 0x1111)
+    P.to_well_formed_batched(x, o, out=w)
+    a = cut - (1 << 20)
+    seg = host(x[a:n])
+    seg_off = np.concatenate([[0], mids - a, [n - 11 - a]]).astype(np.int64)
+    e = O.fix_batched(seg, seg_off)
+    e[n - 11 - a:] = 0x1111                                # units in no string: not written
+    got = host(w[a:n])
+    assert (got[1:] == e[1:]).all()                        # (unit 0 of the window has its real predecessor)
+    assert (host(w[:7]) == 0x1111).all()
+    assert (host(w[7:1 << 20]) == O.fix_batched(host(x[7:(1 << 20) + 1]), np.array([0, (1 << 20) - 6], np.int64))[:(1 << 20) - 7]).all()
+
+
 def test_parts_on_two_streams(P, cuda):
     """INTERIOR and EDGES parts run concurrently on two streams and together
     equal the whole-job repair (the overlap used by dist.repair_shard)."""
