@@ -341,9 +341,12 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if os.environ.get("U16M_BENCH_SHARE_GPU") == "1":
-        # code-path check of the N>1 line on a box with fewer GPUs than ranks
-        # (ranks share devices; the numbers are then meaningless)
+    if os.environ.get("U16M_BENCH_SHARE_GPU") == "1" or local >= torch.cuda.device_count():
+        # U16M_BENCH_SHARE_GPU: code-path check of the N>1 line on a box with
+        # fewer GPUs than ranks (ranks share devices; the numbers are then
+        # meaningless). Otherwise: a launcher that gave every rank its own
+        # CUDA_VISIBLE_DEVICES (one visible GPU, index 0); if ranks really
+        # shared a GPU, NCCL refuses to initialise below.
         local %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
