@@ -23,6 +23,8 @@ for name, fn in (("count_unpaired", lambda: L.u16m_count_unpaired(x.data_ptr(), 
                   lambda: L.u16m_unpaired_offsets(x.data_ptr(), n, 10, offs.data_ptr(), cnt.data_ptr(), s)),
                  ("unpaired_offsets(limit=10), well-formed input",
                   lambda: L.u16m_unpaired_offsets(clean.data_ptr(), n, 10, offs.data_ptr(), cnt.data_ptr(), s)),
+                 ("unpaired_offsets(all), well-formed input",
+                  lambda: L.u16m_unpaired_offsets(clean.data_ptr(), n, n // 16, alloffs.data_ptr(), cnt.data_ptr(), s)),
                  ("unpaired_offsets(all, 8.3M offsets)",
                   lambda: L.u16m_unpaired_offsets(x.data_ptr(), n, n // 16, alloffs.data_ptr(), cnt.data_ptr(), s))):
     tot = 0.0
