@@ -453,7 +453,7 @@ cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long lo
   return launch_stream_count(in, n, count_out, stream);
 }
 
-// Exclusive prefix over per-tile counts in one CTA, 32768 tiles per round:
+// Exclusive prefix over per-tile counts, one CTA per chunk of 32768 tiles:
 // every thread loads its 32 consecutive counts with 8 independent 128-bit
 // loads (the whole round in flight at once), scans them in registers, and a
 // warp-shuffle + shared-memory block scan over the thread totals gives each
@@ -463,14 +463,25 @@ cudaError_t launch_count_unpaired(const uint16_t* in, size_t n, unsigned long lo
 constexpr int kPrefixPer = 32;
 __global__ void __launch_bounds__(1024) tile_prefix_kernel(const uint32_t* counts, uint64_t n,
                                                            unsigned long long* prefix, unsigned long long limit,
-                                                           unsigned long long* count_out) {
+                                                           unsigned long long* count_out,
+                                                           const unsigned long long* chunk_totals) {
   __shared__ unsigned long long warp_tot[32];
   // PDL: the emit grid may launch now; this kernel waits for the counts
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // One CTA per chunk of 32768 counts; the chunks before this one are summed
+  // from the count pass's chunk totals (a single CTA walking 524 288 counts,
+  // config 4's size, took 245 us of a 1.4 ms scan).
   unsigned long long carry = 0;
-  for (uint64_t base = 0; base < n; base += 1024 * kPrefixPer) {
+  for (uint32_t c = 0; c < blockIdx.x; c++) carry += chunk_totals[c];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long total = 0;
+    for (uint32_t c = 0; c < gridDim.x; c++) total += chunk_totals[c];
+    *count_out = total < limit ? total : limit;
+  }
+  {
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * (1024 * kPrefixPer);
     const uint64_t i0 = base + static_cast<uint64_t>(threadIdx.x) * kPrefixPer;
     uint32_t c[kPrefixPer];
     if (i0 + kPrefixPer <= n) {
@@ -493,14 +504,10 @@ __global__ void __launch_bounds__(1024) tile_prefix_kernel(const uint32_t* count
       const unsigned long long y = __shfl_up_sync(kFull, x, o);
       if (lane >= o) x += y;
     }
-    __syncthreads();  // previous round's readers of warp_tot are done
     if (lane == 31) warp_tot[warp] = x;
     __syncthreads();
-    unsigned long long run = carry + x - sum, round_total = 0;
-    for (int w = 0; w < 32; w++) {
-      if (w < warp) run += warp_tot[w];
-      round_total += warp_tot[w];
-    }
+    unsigned long long run = carry + x - sum;
+    for (int w = 0; w < warp; w++) run += warp_tot[w];
     if (i0 + kPrefixPer <= n) {
       ulonglong2* dst = reinterpret_cast<ulonglong2*>(prefix + i0);
 #pragma unroll
@@ -519,16 +526,15 @@ __global__ void __launch_bounds__(1024) tile_prefix_kernel(const uint32_t* count
         run += c[j];
       }
     }
-    carry += round_total;
   }
-  if (threadIdx.x == 0) *count_out = carry < limit ? carry : limit;
 }
 
 cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
                                     unsigned long long* offsets_out, unsigned long long* count_out,
                                     cudaStream_t stream, int32_t left, int32_t right) {
-  cudaError_t e = cudaMemsetAsync(count_out, 0, sizeof(unsigned long long), stream);
-  if (e != cudaSuccess || n == 0 || limit == 0) return e;
+  // (*count_out is always written by tile_prefix_kernel's first CTA)
+  if (n == 0 || limit == 0) return cudaMemsetAsync(count_out, 0, sizeof(unsigned long long), stream);
+  cudaError_t e = cudaSuccess;
   bool same = false;
   const Span s = make_span(in, n, nullptr, left, right, nullptr, nullptr, &same);
   const uint64_t tiles = tiles_for(s);  // 8192-unit tiles of the emit pass
@@ -536,15 +542,23 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   void* ws = nullptr;
   keep_pool_memory();
   const size_t counts_bytes = (halves * sizeof(uint32_t) + 15) / 16 * 16;
-  e = cudaMallocAsync(&ws, counts_bytes + tiles * sizeof(unsigned long long), stream);
+  const uint64_t chunks = (halves + 1024 * kPrefixPer - 1) / (1024 * kPrefixPer);  // 32768 half tiles each
+  const size_t prefix_bytes = (tiles * sizeof(unsigned long long) + 15) / 16 * 16;
+  e = cudaMallocAsync(&ws, counts_bytes + prefix_bytes + chunks * sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   auto* counts = static_cast<uint32_t*>(ws);  // both 16-byte aligned (tile_prefix_kernel)
   auto* prefix = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + counts_bytes);
+  auto* chunk_totals = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + counts_bytes + prefix_bytes);
+  e = cudaMemsetAsync(chunk_totals, 0, chunks * sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(ws, stream);
+    return e;
+  }
   // 1) rewrites per 8192-unit tile: the read-only stream kernel (8 vectors in
   //    flight per thread) writes one count per half of its 16384-unit tile;
   // 2) exclusive prefix + the total; 3) emit on a persistent grid that stops
   //    at the first tile ranked past the limit.
-  e = launch_stream_count(in, n, nullptr, stream, counts, left, right);
+  e = launch_stream_count(in, n, chunk_totals, stream, counts, left, right);
   // (2) and (3) are programmatic dependent launches (PDL): each grid is
   // scheduled while its predecessor runs and waits (griddepcontrol.wait) only
   // for the predecessor's results.
@@ -553,13 +567,14 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   if (e == cudaSuccess) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(1);
+    cfg.gridDim = dim3(static_cast<unsigned>((tiles + 1024 * kPrefixPer - 1) / (1024 * kPrefixPer)));
     cfg.blockDim = dim3(1024);
     cfg.stream = stream;
     cfg.attrs = pdl;
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, tile_prefix_kernel, static_cast<const uint32_t*>(counts), tiles, prefix,
-                           static_cast<unsigned long long>(limit), count_out);
+                           static_cast<unsigned long long>(limit), count_out,
+                           static_cast<const unsigned long long*>(chunk_totals));
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   if (e == cudaSuccess) {

@@ -224,6 +224,9 @@ __global__ void __launch_bounds__(kSThreads, kMinBlocks) stream_kernel(Span s, u
         // (one tile per CTA in this mode; the tile is not blockIdx.x: the last goes first)
         half_tile_counts[2 * count_tile] = c0;
         half_tile_counts[2 * count_tile + 1] = c1;
+        // ... and the total of every chunk of 32768 half tiles (count[chunk]), so
+        // that tile_prefix_kernel can scan the chunks in parallel, one CTA each
+        if (count && (c0 | c1)) atomicAdd(count + (count_tile >> 14), static_cast<unsigned long long>(c0) + c1);
       } else {
         unsigned long long c = 0;
 #pragma unroll
@@ -816,7 +819,8 @@ cudaError_t launch_stream_codec(const Span& s, bool big_endian, unsigned long lo
 // Validation (§8(f-1)): the stream kernel with the count and no stores —
 // 2 B/unit read-only, one tile per CTA. With half_tile_counts set it writes
 // the rewrite count of every 8192-unit half tile instead of the total
-// (2 * ceil(n_vectors / 2048) entries).
+// (2 * ceil(n_vectors / 2048) entries), and `count` (if set) is an array of
+// totals per chunk of 32768 half tiles (zeroed by the caller).
 cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long* count, cudaStream_t stream,
                                 uint32_t* half_tile_counts, int32_t left, int32_t right) {
   if (n == 0) return cudaSuccess;
