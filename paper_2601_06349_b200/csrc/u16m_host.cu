@@ -448,10 +448,10 @@ cudaError_t ensure_small(HostPipe* p) {
   cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p->small), kSmallUnits * sizeof(uint16_t) + 64,
                                 cudaHostAllocMapped);
   if (e == cudaSuccess)
-    e = cudaHostAlloc(reinterpret_cast<void**>(&p->small_count), sizeof(unsigned long long), cudaHostAllocDefault);
+    e = cudaHostAlloc(reinterpret_cast<void**>(&p->small_count), sizeof(unsigned long long), cudaHostAllocMapped);
   if (e == cudaSuccess)
     e = cudaHostAlloc(reinterpret_cast<void**>(&p->small_offs), kSmallOffs * sizeof(unsigned long long),
-                      cudaHostAllocDefault);
+                      cudaHostAllocMapped);
   if (e == cudaSuccess) e = cudaMalloc(&p->small_dev, (kSmallUnits + 8) * sizeof(unsigned long long));
   if (e != cudaSuccess) {
     if (p->small) cudaFreeHost(p->small);
@@ -751,14 +751,23 @@ u16m_status unpaired_offsets_host(const uint16_t* in, size_t n, int byte_order, 
       if (e != cudaSuccess) return cuda_fail(e, "small scan staging");
       din = static_cast<const uint16_t*>(d);
     }
+    // limit <= kSmallOffs (is_well_formed asks for 1, the CLI for 10): the scan
+    // kernel writes the count and the offsets straight into mapped pinned host
+    // memory — one launch and one synchronisation, no device-to-host copies.
+    const bool one_sync = limit <= kSmallOffs;
     unsigned long long* d_off = p->small_dev;
     unsigned long long* d_cnt = p->small_dev + kSmallUnits;
+    if (one_sync) {
+      void *mo = nullptr, *mc = nullptr;
+      e = cudaHostGetDevicePointer(&mo, p->small_offs, 0);
+      if (e == cudaSuccess) e = cudaHostGetDevicePointer(&mc, p->small_count, 0);
+      if (e != cudaSuccess) return cuda_fail(e, "small scan output mapping");
+      d_off = static_cast<unsigned long long*>(mo);
+      d_cnt = static_cast<unsigned long long*>(mc);
+    }
     e = u16m::launch_unpaired_offsets(din, n, limit, d_off, d_cnt, p->comp, -1, -1);
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && !one_sync)
       e = cudaMemcpyAsync(p->small_count, d_cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->comp);
-    const bool one_sync = limit <= kSmallOffs;
-    if (e == cudaSuccess && one_sync)
-      e = cudaMemcpyAsync(p->small_offs, d_off, limit * sizeof(unsigned long long), cudaMemcpyDeviceToHost, p->comp);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->comp);
     if (e != cudaSuccess) return cuda_fail(e, "small scan");
     const size_t cnt = static_cast<size_t>(*p->small_count);

@@ -77,6 +77,12 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
                                     unsigned long long* offsets_out, unsigned long long* count_out,
                                     cudaStream_t stream, int32_t left = -1, int32_t right = -1);
 
+// Short buffers (0 < n <= kSmallScanUnits, limit > 0): the whole offsets scan
+// in one single-CTA launch (u16m_stream.cu).
+constexpr size_t kSmallScanUnits = size_t(64) << 10;
+cudaError_t launch_small_scan(const uint16_t* in, size_t n, size_t limit, unsigned long long* offsets_out,
+                              unsigned long long* count_out, cudaStream_t stream, int32_t left, int32_t right);
+
 // In-place byte swap of n units (p 16-byte aligned).
 cudaError_t launch_byteswap(uint16_t* p, size_t n, cudaStream_t stream);
 

@@ -534,6 +534,7 @@ cudaError_t launch_unpaired_offsets(const uint16_t* in, size_t n, size_t limit,
                                     cudaStream_t stream, int32_t left, int32_t right) {
   // (*count_out is always written by tile_prefix_kernel's first CTA)
   if (n == 0 || limit == 0) return cudaMemsetAsync(count_out, 0, sizeof(unsigned long long), stream);
+  if (n <= kSmallScanUnits) return launch_small_scan(in, n, limit, offsets_out, count_out, stream, left, right);
   cudaError_t e = cudaSuccess;
   bool same = false;
   const Span s = make_span(in, n, nullptr, left, right, nullptr, nullptr, &same);

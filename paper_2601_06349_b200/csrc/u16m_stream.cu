@@ -852,6 +852,134 @@ cudaError_t launch_stream_count(const uint16_t* in, size_t n, unsigned long long
   return cudaGetLastError();
 }
 
+// ---- small offsets scans: one launch ----------------------------------------
+// unpaired_surrogate_offsets / is_well_formed on a short buffer (a Python
+// string, a small file: n <= kSmallScanUnits) is all launch latency: the
+// count -> prefix -> emit chain is three launches plus a workspace
+// allocation. Here ONE CTA walks the buffer in 16384-unit tiles (8 x 128-bit
+// loads in flight per thread, the stream kernel's layout), ranks each tile's
+// rewrites behind a running total and writes the ascending offsets and
+// min(total, limit) itself; it stops at the tile that completes the limit.
+// Every tile takes the guarded (edge) path: at this size the range tests cost
+// nothing measurable.
+__global__ void __launch_bounds__(kSThreads, 1) small_scan_kernel(Span s, unsigned long long limit,
+                                                                  unsigned long long* offsets_out,
+                                                                  unsigned long long* count_out) {
+  __shared__ uint32_t warp_tot[kSThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t vbeg = s.lo / 8;
+  const uint64_t vend = (s.hi + 7) / 8;
+  const uint64_t ntiles = (vend - vbeg + kSCtaVecs - 1) / kSCtaVecs;
+  unsigned long long base = 0;  // rewrites in the tiles before this one (CTA-uniform)
+  for (uint64_t tile = 0; tile < ntiles && base < limit; tile++) {
+    const uint64_t wv0 = vbeg + tile * kSCtaVecs + static_cast<uint64_t>(warp) * kSWarpVecs;
+    const uint64_t v0 = wv0 + lane;
+    uint4 v[kSV];
+#pragma unroll
+    for (int k = 0; k < kSV; k++) {
+      const uint64_t vi = v0 + k * 32;
+      v[k] = vi < vend ? ld_stream(s.in + vi) : make_uint4(0, 0, 0, 0);
+    }
+    uint32_t halo = 0;
+    if (lane == 0) halo = unit_at(s, static_cast<int64_t>(wv0 * 8) - 1);
+    if (lane == 31) halo = unit_at(s, static_cast<int64_t>((wv0 + kSWarpVecs) * 8));
+#pragma unroll
+    for (int k = 0; k < kSV; k++) {
+      const uint64_t vi = v0 + k * 32;
+      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) patch_edges(s, vi, v[k]);
+    }
+    uint32_t B0[kSV], B1[kSV];
+    {
+      Flags cur = classify8(v[0]);
+      uint32_t hp_carry = hflag_hi(halo);
+      const uint32_t halo_l = lflag_lo(halo);
+      const int up_lane = (lane + 31) & 31, dn_lane = (lane + 1) & 31;
+#pragma unroll
+      for (int k = 0; k < kSV; k++) {
+        Flags nxt;
+        if (k + 1 < kSV) nxt = classify8(v[k + 1]);
+        const uint32_t up = __shfl_sync(kFull, cur.H1, up_lane);
+        const uint32_t dn = __shfl_sync(kFull, cur.L0, dn_lane);
+        uint32_t ln = dn;
+        if (k + 1 < kSV) {
+          const uint32_t dn_next = __shfl_sync(kFull, nxt.L0, dn_lane);
+          if (lane == 31) ln = dn_next;
+        } else if (lane == 31) {
+          ln = halo_l;
+        }
+        const uint32_t hp = lane ? up : hp_carry;
+        hp_carry = up;
+        bad8(cur, hp, ln, B0[k], B1[k]);
+        if (k + 1 < kSV) cur = nxt;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kSV; k++) {
+      const uint64_t vi = v0 + k * 32;
+      if (vi * 8 < s.lo || vi * 8 + 8 > s.hi) mask_outside(s, vi, B0[k], B1[k]);
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < kSV; k++) mine += __popc(B0[k]) + __popc(B1[k]);
+    const uint32_t warp_count = __reduce_add_sync(kFull, mine);
+    __syncthreads();  // the previous tile's readers of warp_tot are done
+    if (lane == 0) warp_tot[warp] = warp_count;
+    __syncthreads();
+    uint32_t total = 0, before = 0;
+#pragma unroll
+    for (int w = 0; w < kSThreads / 32; w++) {
+      total += warp_tot[w];
+      if (w < warp) before += warp_tot[w];
+    }
+    if (warp_count != 0 && base + before < limit) {
+      // ranks follow unit order: warp, then row k, then lane
+      uint32_t run = 0;
+#pragma unroll
+      for (int k = 0; k < kSV; k++) {
+        const uint32_t c = __popc(B0[k]) + __popc(B1[k]);
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        unsigned long long r = base + before + run + x - c;
+        run += __shfl_sync(kFull, x, 31);
+        const uint64_t a0 = (v0 + k * 32) * 8 - s.lo;
+        uint64_t bits = static_cast<uint64_t>(B0[k]) | (static_cast<uint64_t>(B1[k]) << 32);
+        while (bits && r < limit) {
+          const int bit = __ffsll(static_cast<long long>(bits)) - 1;
+          bits &= bits - 1;
+          offsets_out[r++] = a0 + (bit >> 3);
+        }
+      }
+    }
+    base += total;
+  }
+  if (threadIdx.x == 0) *count_out = base < limit ? base : limit;
+}
+
+// n in (0, kSmallScanUnits], limit > 0.
+cudaError_t launch_small_scan(const uint16_t* in, size_t n, size_t limit, unsigned long long* offsets_out,
+                              unsigned long long* count_out, cudaStream_t stream, int32_t left, int32_t right) {
+  const uintptr_t ia = reinterpret_cast<uintptr_t>(in);
+  const uint32_t ph = static_cast<uint32_t>((ia & 15u) / 2);
+  Span s;
+  s.in = reinterpret_cast<const uint4*>(ia - 2 * ph);
+  s.out = nullptr;
+  s.out_units = nullptr;
+  s.lo = ph;
+  s.hi = ph + n;
+  s.left = left;
+  s.right = right;
+  s.left_ptr = s.right_ptr = nullptr;
+  s.tile_sel = kTilesAll;
+  s.prefetch_tiles = 0;
+  small_scan_kernel<<<1, kSThreads, 0, stream>>>(s, static_cast<unsigned long long>(limit), offsets_out, count_out);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // Copy with out at a different 16-byte phase than in (see stream_shift_kernel).
 template <bool kBE, bool kCount>
 static cudaError_t launch_shift_t(Span s, uint16_t* out, int part, unsigned long long* count, cudaStream_t stream) {

@@ -209,6 +209,35 @@ def test_count_and_offsets(P, cuda):
     assert P.unpaired_surrogate_offsets(O.u16([0x41, 0xDC00, 0x42, 0xD800]).tobytes(), 1) == [1]
 
 
+def test_offsets_small_scan_threshold(P, cuda):
+    """Buffers of up to 64 Ki units take the single-launch scan (one CTA walks
+    the tiles), longer ones the count -> prefix -> emit chain: lengths on both
+    sides of the switch and of the 16384-unit tile edges, every 16-byte phase,
+    limits that stop inside the first, a middle and the last tile, dense and
+    sparse rewrites, clean input."""
+    rng = np.random.default_rng(77)
+    big = rng.choice(ALPHABET, (1 << 16) + 64 + 8)
+    sparse = np.full(big.size, 0x41, np.uint16)
+    sparse[rng.integers(0, big.size, 40)] = 0xDC00
+    for src in (big, sparse):
+        t_all = dev(src)
+        for n in (16383, 16384, 16385, 32768 + 5, 65535, 65536, 65537, 65536 + 64):
+            for ph in (0, 1, 3, 7):
+                x = src[ph:ph + n]
+                e = O.unpaired_offsets(x)
+                t = t_all[ph:ph + n]
+                assert P.count_unpaired(t) == len(e)
+                assert P.unpaired_offsets_device(t).cpu().tolist() == e, (n, ph)
+                for lim in (1, 10, len(e) // 2, len(e), len(e) + 5):
+                    assert P.unpaired_offsets_device(t, lim).cpu().tolist() == e[:lim], (n, ph, lim)
+    clean = torch.full((65536,), 0x41, dtype=torch.int16, device="cuda")
+    assert P.unpaired_offsets_device(clean, 10).numel() == 0
+    # the host scan of a short buffer (mapped pinned memory read by the same kernel)
+    b = big[:50_001].tobytes()
+    assert P.unpaired_surrogate_offsets(b) == O.unpaired_offsets(big[:50_001])
+    assert P.unpaired_surrogate_offsets(b, 3) == O.unpaired_offsets(big[:50_001], 3)
+
+
 def test_offsets_many_tiles(P, cuda):
     """unpaired offsets over more than one round of the single-CTA tile prefix
     (32768 tiles of 8192 units): lone surrogates planted at known places in an
