@@ -56,6 +56,7 @@ struct HostPipe {
   cudaEvent_t loaded[kRing] = {}, repaired[kRing] = {}, drained[kRing] = {};
   uint16_t* stage[kStage] = {};           // pinned, allocated on the first pageable job
   cudaEvent_t staged[kStage] = {};
+  unsigned long long* stage_total = nullptr;  // pinned [kStage]: the counter after each staged chunk's kernel
   uint16_t* small = nullptr;              // pinned + mapped, small jobs (kSmallUnits), lazily
   unsigned long long* small_count = nullptr;  // pinned, the small path's count read-back
   unsigned long long* small_offs = nullptr;   // pinned, small scans' offsets read-back (kSmallOffs)
@@ -315,9 +316,14 @@ cudaError_t d2h_staged(HostPipe* p, void* dst, const void* src, size_t bytes) {
 // buffers: per chunk H2D -> compute(dbuf, c0, len) on p->comp -> D2H. The
 // chunks may have any lengths up to pipe_chunk_units(). The calling thread
 // must have made p->device current and hold p->mu.
+// track_clean (pageable in-place jobs whose kernels add their rewrites to
+// p->counter, reset by the caller): a chunk without rewrites is not copied
+// back — `out` is `in` and already holds it — which halves the host copy
+// work, the limit of pageable jobs, on clean text.
 template <class Compute>
 u16m_status pipeline_chunks(HostPipe* p, const uint16_t* in, uint16_t* out,
-                            const std::vector<std::pair<size_t, size_t>>& chunks, Compute compute) {
+                            const std::vector<std::pair<size_t, size_t>>& chunks, Compute compute,
+                            bool track_clean = false) {
   cudaError_t e = cudaSuccess;
   // Pageable host memory: the copy engines cannot DMA it directly, so every
   // chunk is copied (by the CopyPool threads) into a pinned bounce buffer,
@@ -328,10 +334,23 @@ u16m_status pipeline_chunks(HostPipe* p, const uint16_t* in, uint16_t* out,
   if (!is_pinned(in) || !is_pinned(out)) {
     CopyPool& pool = CopyPool::get();
     const size_t nchunks = chunks.size();
+    const bool skip_clean = track_clean && in == out;
+    if (skip_clean && p->stage_total == nullptr) {
+      e = cudaHostAlloc(reinterpret_cast<void**>(&p->stage_total), kStage * sizeof(unsigned long long),
+                        cudaHostAllocDefault);
+      if (e != cudaSuccess) return cuda_fail(e, "staging buffers");
+    }
+    unsigned long long seen_total = 0;  // p->counter after the last chunk copied out (chunks drain in order)
     auto copy_out = [&](size_t c) -> cudaError_t {
       const int k = static_cast<int>(c % kStage);
       const cudaError_t r = cudaEventSynchronize(p->staged[k]);
       if (r != cudaSuccess) return r;
+      if (skip_clean) {
+        const unsigned long long total = p->stage_total[k];
+        const bool clean = total == seen_total;
+        seen_total = total;
+        if (clean) return cudaSuccess;  // nothing was rewritten: the caller's buffer already holds this chunk
+      }
       pool.copy(out + chunks[c].first, p->stage[k], chunks[c].second * sizeof(uint16_t));
       return cudaSuccess;
     };
@@ -352,6 +371,11 @@ u16m_status pipeline_chunks(HostPipe* p, const uint16_t* in, uint16_t* out,
       cudaStreamWaitEvent(p->comp, p->loaded[k], 0);
       e = compute(p->dbuf[k], c0, len);
       if (e != cudaSuccess) return cuda_fail(e, "repair kernel launch");
+      if (skip_clean) {  // the running rewrite count after this chunk (complete before staged[k])
+        e = cudaMemcpyAsync(p->stage_total + k, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            p->comp);
+        if (e != cudaSuccess) return cuda_fail(e, "chunk rewrite count");
+      }
       cudaEventRecord(p->repaired[k], p->comp);
       cudaStreamWaitEvent(p->d2h, p->repaired[k], 0);
       e = cudaMemcpyAsync(p->stage[k], p->dbuf[k], len * 2, cudaMemcpyDeviceToHost, p->d2h);
@@ -416,14 +440,15 @@ u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out,
     // when no neighbour pairs with it).
     const int32_t left = c0 > 0 ? unit(c0 - 1) : -1;
     const int32_t right = c0 + len < n ? unit(c0 + len) : -1;
-    return byte_order < 0 ? u16m::launch_repair(d, len, d, left, right, nullptr, nullptr, p->comp)
-                          : u16m::launch_fix_bytes(d, len, d, be, count ? p->counter : nullptr, p->comp, left, right);
+    if (byte_order < 0 && !count)
+      return u16m::launch_repair(d, len, d, left, right, nullptr, nullptr, p->comp);
+    return u16m::launch_fix_bytes(d, len, d, be, count ? p->counter : nullptr, p->comp, left, right);
   };
   const size_t chunk = pipe_chunk_units();
   std::vector<std::pair<size_t, size_t>> chunks;
   chunks.reserve((b - a + chunk - 1) / chunk);
   for (size_t c0 = a; c0 < b; c0 += chunk) chunks.emplace_back(c0, std::min(chunk, b - c0));
-  return pipeline_chunks(p, in, out, chunks, repair);
+  return pipeline_chunks(p, in, out, chunks, repair, /*track_clean=*/count);
 }
 
 // Device-accessible address of pinned (page-locked, mapped) host memory, or
@@ -505,11 +530,14 @@ u16m_status host_device_job(int dev, const uint16_t* in, size_t n, uint16_t* out
   if (p == nullptr) return st;
   std::lock_guard<std::mutex> lock(p->mu);  // one staged job per device at a time
   if (a == 0 && b == n && n <= kSmallUnits) return host_small(p, in, n, out, byte_order, replacements);
-  if (replacements) {
+  // Pageable in-place jobs count their rewrites even when the caller does not
+  // ask for the count: chunks without any are not copied back (pipeline_chunks).
+  const bool count = replacements != nullptr || (in == out && !is_pinned(in));
+  if (count) {
     e = cudaMemsetAsync(p->counter, 0, sizeof(unsigned long long), p->comp);
     if (e != cudaSuccess) return cuda_fail(e, "counter reset");
   }
-  st = host_range(p, in, n, out, a, b, byte_order, replacements != nullptr);
+  st = host_range(p, in, n, out, a, b, byte_order, count);
   if (st == U16M_OK && replacements) {
     e = cudaMemcpy(replacements, p->counter, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(e, "replacement count");

@@ -366,6 +366,21 @@ def test_host_pipeline_chunks(P, cuda):
     assert (pg.view(np.uint16) == ey).all()
 
 
+@pytest.mark.parametrize("chunk_kib", ["64", "1024"])
+def test_host_pageable_inplace_skips_clean_chunks(cuda, chunk_kib):
+    """Pageable in-place host jobs do not copy clean chunks back; results and
+    replacement counts stay exact for every placement of the dirty chunks
+    (helper process: the chunk size is read once per process)."""
+    import subprocess
+    import sys
+
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gpu_helpers", "host_clean_chunks_check.py")
+    env = {k: v for k, v in os.environ.items() if not k.startswith("U16M_")}
+    env["U16M_PIPE_CHUNK_KIB"] = chunk_kib
+    r = subprocess.run([sys.executable, helper], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
 def test_sharded_virtual(P, cuda):
     """u16m_to_well_formed_sharded with several shards on one GPU (device ids
     repeat), including empty shards and adversarial shard-edge patterns."""
