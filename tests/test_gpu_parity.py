@@ -232,6 +232,20 @@ def test_offsets_small_scan_threshold(P, cuda):
                     assert P.unpaired_offsets_device(t, lim).cpu().tolist() == e[:lim], (n, ph, lim)
     clean = torch.full((65536,), 0x41, dtype=torch.int16, device="cuda")
     assert P.unpaired_offsets_device(clean, 10).numel() == 0
+    # nothing is written past `limit` entries (guard region behind offsets_out), both paths
+    L = P._lib.raw()
+    s0 = torch.cuda.current_stream().cuda_stream
+    for n in (50_000, 65536 + 64):
+        x = big[:n]
+        e = O.unpaired_offsets(x)
+        t = dev(x)
+        for lim in (1, 10, 333, len(e)):
+            buf = torch.full((lim + 64,), -7, dtype=torch.int64, device="cuda")
+            cnt = torch.full((3,), -7, dtype=torch.int64, device="cuda")
+            assert L.u16m_unpaired_offsets(t.data_ptr(), n, lim, buf.data_ptr(), cnt[1:].data_ptr(), s0) == 0
+            torch.cuda.synchronize()
+            assert cnt.tolist() == [-7, min(lim, len(e)), -7]
+            assert buf[:lim].tolist() == e[:lim] and (buf[lim:] == -7).all(), (n, lim)
     # the host scan of a short buffer (mapped pinned memory read by the same kernel)
     b = big[:50_001].tobytes()
     assert P.unpaired_surrogate_offsets(b) == O.unpaired_offsets(big[:50_001])
