@@ -378,7 +378,7 @@ def _host_offsets(data, limit: int) -> list[int]:
     out = np.empty(cap, dtype=np.uint64)
     cnt = ctypes.c_size_t(0)
     _check(_L.u16m_unpaired_offsets_host(src.ctypes.data, n, cap, out.ctypes.data, ctypes.byref(cnt)))
-    return [int(v) for v in out[: cnt.value]]
+    return out[: cnt.value].tolist()
 
 
 def is_well_formed_utf16le(data) -> bool:
