@@ -633,6 +633,10 @@ def run_ours(args):
             log("cpu baseline failed:", e)
 
     if distributed:
+        # release the neighbours' IPC mappings before any producer exits
+        used_ipc = bool(halos)
+        halos.clear()
+        torch.cuda.synchronize()
         dist.barrier()
         dist.destroy_process_group()
     if rank != 0:
@@ -658,7 +662,7 @@ def run_ours(args):
         "data": "synthetic",
         "config": config_dict(args.config, units, world) if not args.units else
         {**config_dict(args.config, units, world), "workload": desc + f" (REDUCED: {units} units/GPU)"},
-        "run": {"halo": ((("ipc-peer-loads" if halos else "nccl-allgather")) if distributed else None),
+        "run": {"halo": ((("ipc-peer-loads" if used_ipc else "nccl-allgather")) if distributed else None),
                 "warm": bool(args.warm)},
         "roofline": head_sum["roofline"],
         "modes": {m: {**s, **({"e2e": e2e[m]} if m in e2e else {})} for m, (_, s) in summaries.items()},
