@@ -187,9 +187,10 @@ static float run(const Ctx& c, int reps) {
   return ms[ms.size() / 2] * 1e3f;
 }
 
+static int g_mode = 0;  // 0: dirty sectors only (in place); 2: every vector rewritten (copy-like traffic)
 template <int LP, int SP>
 static void row(const Ctx& c, int reps, const char* tag) {
-  const float t = run<LP, SP, 0>(c, reps);
+  const float t = g_mode == 2 ? run<LP, SP, 2>(c, reps) : run<LP, SP, 0>(c, reps);
   printf("%-6s %-22s %-24s %10.1f us  %7.1f GB/s input\n", tag, kLdName[LP], kStName[SP], t,
          c.nvec * 16.0 / (t * 1e-6) / 1e9);
   fflush(stdout);
@@ -223,6 +224,7 @@ static int sweep(const Ctx& c, int reps, const char* tag) {
 
 int main(int argc, char** argv) {
   const int reps = argc > 1 ? atoi(argv[1]) : 9;
+  g_mode = argc > 2 ? atoi(argv[2]) : 0;
   Ctx c;
   c.flvec = (512u << 20) / 16;
   CK(cudaMalloc(&c.fl, c.flvec * 16));
