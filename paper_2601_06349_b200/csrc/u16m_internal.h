@@ -83,6 +83,9 @@ constexpr size_t kSmallScanUnits = size_t(64) << 10;
 cudaError_t launch_small_scan(const uint16_t* in, size_t n, size_t limit, unsigned long long* offsets_out,
                               unsigned long long* count_out, cudaStream_t stream, int32_t left, int32_t right);
 
+// *dst_mapped (mapped pinned host memory, device address) = *src (device), stream-ordered, no copy engine.
+cudaError_t launch_store_u64(unsigned long long* dst_mapped, const unsigned long long* src, cudaStream_t stream);
+
 // In-place byte swap of n units (p 16-byte aligned).
 cudaError_t launch_byteswap(uint16_t* p, size_t n, cudaStream_t stream);
 

@@ -1047,6 +1047,20 @@ __global__ void byteswap_kernel(uint4* __restrict__ p, uint64_t nvec, uint16_t* 
   }
 }
 
+// *dst = *src, dst in mapped pinned host memory: how the host pipelines read a
+// device counter between chunks without a copy-engine transfer (an 8-byte
+// cudaMemcpyAsync queues behind the 64 MiB chunk copies on the same engine and
+// stalled the kernels behind it: -4 % on error-dense input).
+// (no system fence: the host reads after synchronising on an event recorded
+// behind this kernel, which orders the posted write before the completion)
+__global__ void store_u64_kernel(unsigned long long* dst, const unsigned long long* src) { *dst = *src; }
+
+cudaError_t launch_store_u64(unsigned long long* dst_mapped, const unsigned long long* src, cudaStream_t stream) {
+  store_u64_kernel<<<1, 1, 0, stream>>>(dst_mapped, src);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_byteswap(uint16_t* p, size_t n, cudaStream_t stream) {
   if (n == 0) return cudaSuccess;
   const uint64_t nvec = n / 8;
