@@ -34,6 +34,11 @@ namespace {
 constexpr int kRing = 8;
 constexpr size_t kChunkUnits = size_t(32) << 20;  // largest chunk: 64 MiB
 
+bool pipe_chunk_override() {
+  static const bool o = std::getenv("U16M_PIPE_CHUNK_KIB") != nullptr;
+  return o;
+}
+
 // Pipeline chunk in units (U16M_PIPE_CHUNK_KIB overrides; at most kChunkUnits).
 size_t pipe_chunk_units() {
   static const size_t c = [] {
@@ -45,6 +50,22 @@ size_t pipe_chunk_units() {
   }();
   return c;
 }
+
+// Chunk of a plain / byte-order-fused host job over `units` units. Pinned
+// buffers of 2 GiB and more stream in 64 MiB chunks: the DMA engines idle for
+// the kernel + event latency between a chunk's H2D and its D2H, and with the
+// two directions sharing ~96 GB/s every idle microsecond costs 0.4; fewer,
+// larger chunks halve that (8 GiB: 48.1 -> 48.6 GB/s; 128 MiB the same, 256 MiB
+// 47.7). Smaller jobs keep 32 MiB (512 MiB: 46.1 against 44.8 at 64 MiB — the
+// unoverlapped first H2D and last D2H weigh more), pageable jobs too (their
+// bounce buffers are pinned memory: 4 x chunk).
+size_t job_chunk_units(size_t units, bool pinned) {
+  if (pipe_chunk_override() || !pinned) return pipe_chunk_units();
+  return units >= (size_t(1) << 30) ? kChunkUnits : pipe_chunk_units();
+}
+
+// Device ring slots hold the largest chunk a job may use.
+size_t ring_slot_units() { return pipe_chunk_override() ? pipe_chunk_units() : kChunkUnits; }
 
 constexpr int kStage = 4;  // pinned bounce buffers for pageable host jobs
 
@@ -233,7 +254,7 @@ HostPipe* pipe_for(int device, u16m_status* st) {
 // of 32 MiB alone takes tens of ms).
 cudaError_t ensure_dbuf(HostPipe* p, int k) {
   if (p->dbuf[k]) return cudaSuccess;
-  return cudaMalloc(&p->dbuf[k], pipe_chunk_units() * sizeof(uint16_t));
+  return cudaMalloc(&p->dbuf[k], ring_slot_units() * sizeof(uint16_t));
 }
 
 cudaError_t ensure_stage(HostPipe* p, int k) {
@@ -408,7 +429,8 @@ u16m_status pipeline_pinned_inplace(HostPipe* p, uint16_t* buf, const std::vecto
 
 // The staged copy-engine pipeline over a list of unit ranges of the caller's
 // buffers: per chunk H2D -> compute(dbuf, c0, len) on p->comp -> D2H. The
-// chunks may have any lengths up to pipe_chunk_units(). The calling thread
+// chunks may have any lengths up to ring_slot_units() (pageable buffers: up to
+// pipe_chunk_units(), the size of the bounce buffers). The calling thread
 // must have made p->device current and hold p->mu.
 // track_clean (pageable in-place jobs whose kernels add their rewrites to
 // p->counter, reset by the caller): a chunk without rewrites is not copied
@@ -543,9 +565,11 @@ u16m_status host_range(HostPipe* p, const uint16_t* in, size_t n, uint16_t* out,
       return u16m::launch_repair(d, len, d, left, right, nullptr, nullptr, p->comp);
     return u16m::launch_fix_bytes(d, len, d, be, count ? p->counter : nullptr, p->comp, left, right);
   };
-  const size_t chunk = pipe_chunk_units();
+  const size_t chunk = job_chunk_units(b - a, is_pinned(in) && is_pinned(out));
   std::vector<std::pair<size_t, size_t>> chunks;
   chunks.reserve((b - a + chunk - 1) / chunk);
+  // (a ramp of smaller chunks at the head and tail — the only transfers nothing
+  // overlaps — measured +0.1 %, within noise: profiles/r02/ab_host_chunk_size.txt)
   for (size_t c0 = a; c0 < b; c0 += chunk) chunks.emplace_back(c0, std::min(chunk, b - c0));
   return pipeline_chunks(p, in, out, chunks, repair, /*track_clean=*/count);
 }
